@@ -1,0 +1,547 @@
+#!/usr/bin/env python3
+"""bench.py -- Merge Path on B200: the BASELINE.json headline metric.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2]
+    python bench.py --impl reference ...     # the reference's CPU path
+
+Default workload (BASELINE.json configs[1], the merge the metric is quoted
+on): stable merge of two sorted int32 arrays, |A| = |B| = 2^28, keys
+uniform in [0,1024) from seeds 1 (A) and 2 (B) (SURVEY.md §8d generator).
+A "step" is one pass of the hot path (K1 tile partition + K2 tile merge)
+over that input, resident in HBM.  Inputs (2 GiB) and output (2 GiB) are
+far larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  `value` = merged elements/s over all ranks,
+device-timed with CUDA events, max over ranks; `e2e` = the same metric
+through the public C ABI with host (pinned) buffers, H2D + D2H included;
+`roofline` = the tile-merge kernel's algorithmic bytes / its average
+CUDA-event duration vs the measured HBM peak; `cpu_baseline` = the
+reference's own parallel_merge_into (oracle/_ref) on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, only if the file is absent
+
+
+def load_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------
+# workloads
+# --------------------------------------------------------------------------
+CONFIGS = {
+    "1": dict(kind="merge", key="u32", gen=(0, 0), na=1 << 20, nb=1 << 20, bytes_per=8,
+              desc="config1: stable merge u32 |A|=|B|=2^20, seeds 1/2"),
+    "2": dict(kind="merge", key="i32", gen=(1, 1), na=1 << 28, nb=1 << 28, bytes_per=8,
+              desc="config2: stable merge i32 |A|=|B|=2^28, keys uniform in [0,1024), seeds 1/2"),
+    "3a": dict(kind="merge", key="u64", gen=(2, 2), na=1 << 29, nb=1 << 25, bytes_per=24, vals=True,
+               desc="config3a: stable merge u64 key + u32 value, |A|=2^29 |B|=2^25, uniform keys"),
+    "3b": dict(kind="merge", key="u64", gen=(4, 3), na=1 << 29, nb=1 << 25, bytes_per=24, vals=True,
+               desc="config3b: stable merge u64 key + u32 value, |A|=2^29 |B|=2^25, B below A"),
+    "4": dict(kind="sort", key="u32", gen=(0, None), n=1 << 30, bytes_per=160,
+              desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 2048-key block sort + 19 rounds"),
+}
+KT = {"u32": 0, "i32": 1, "f32": 2, "u64": 3, "i64": 4}
+KSIZE = {"u32": 4, "i32": 4, "f32": 4, "u64": 8, "i64": 8}
+
+
+def torch_dtype(torch, key):
+    return {"u32": torch.uint32, "i32": torch.int32, "u64": torch.uint64,
+            "i64": torch.int64, "f32": torch.float32}[key]
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML while running."""
+
+    BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+           "hw_power_brake_slowdown": 0x80}
+    NOTED = {"sw_power_cap": 0x4}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in {**self.BAD, **self.NOTED}.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------
+# distributed plumbing
+# --------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def barrier(dist_on):
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, dist_on: bool) -> float:
+    if not dist_on:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def make_inputs(torch, N, cfg, dev, stream):
+    """Generate the config's inputs on the device (same bytes as the oracle
+    generator, tests/test_gpu_parity.py) and sort them with our own sort
+    (not timed)."""
+    key = cfg["key"]
+    dt = torch_dtype(torch, key)
+    kt = KT[key]
+    s = stream.cuda_stream
+
+    def gen(kind, seed, n):
+        x = torch.empty(n, dtype=dt, device=dev)
+        N.check(N.lib.mp_generate(kind, seed, 0, n, x.data_ptr(), s))
+        return x
+
+    if cfg["kind"] == "sort":
+        return gen(cfg["gen"][0], 4, cfg["n"])
+    a = gen(cfg["gen"][0], 1, cfg["na"])
+    b = gen(cfg["gen"][1], 2, cfg["nb"])
+    for x in (a, b):
+        N.check(N.lib.mp_sort(kt, x.data_ptr(), None, x.numel(), None, 0, s))
+    av = bv = None
+    if cfg.get("vals"):
+        av = torch.arange(cfg["na"], dtype=torch.int32, device=dev).view(torch.uint32)
+        bv = (torch.arange(cfg["nb"], dtype=torch.int32, device=dev)
+              + torch.iinfo(torch.int32).min).view(torch.uint32)
+    return a, b, av, bv
+
+
+def run_ours(args, cfg, ws, rank, local, dist_on):
+    import torch
+    from paper_1406_2628_b200 import _native as N
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    peak, peak_src = load_peak()
+    key, kt = cfg["key"], KT[cfg["key"]]
+    launches = 0
+    with torch.cuda.stream(stream):
+        if cfg["kind"] == "merge":
+            a, b, av, bv = make_inputs(torch, N, cfg, dev, stream)
+            na, nb = a.numel(), b.numel()
+            n = na + nb
+            out = torch.empty(n, dtype=a.dtype, device=dev)
+            outv = torch.empty(n, dtype=torch.uint32, device=dev) if av is not None else None
+            wsb = N.lib.mp_merge_workspace_bytes(kt, na, nb)
+            wsp = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
+            ptr = (lambda t: t.data_ptr() if t is not None else None)
+
+            def step(evs=None):
+                N.check(N.lib.mp_merge_plan(kt, a.data_ptr(), na, b.data_ptr(), nb,
+                                            wsp.data_ptr(), stream.cuda_stream))
+                if evs is not None:
+                    evs[0].record(stream)
+                N.check(N.lib.mp_merge_execute(kt, a.data_ptr(), ptr(av), na, b.data_ptr(),
+                                               ptr(bv), nb, out.data_ptr(), ptr(outv),
+                                               wsp.data_ptr(), stream.cuda_stream))
+                if evs is not None:
+                    evs[1].record(stream)
+            launches_per_step = 2
+            units = n
+        else:
+            data0 = make_inputs(torch, N, cfg, dev, stream)
+            n = data0.numel()
+            data = torch.empty_like(data0)
+            scratch_b = N.lib.mp_sort_scratch_bytes(kt, 0, n)
+            scratch = torch.empty(scratch_b, dtype=torch.uint8, device=dev)
+
+            def step(evs=None):
+                # each step sorts a fresh copy of the unsorted keys; the copy
+                # is outside the kernel events but inside the step time
+                data.copy_(data0)
+                if evs is not None:
+                    evs[0].record(stream)
+                N.check(N.lib.mp_sort(kt, data.data_ptr(), None, n, scratch.data_ptr(),
+                                      scratch_b, stream.cuda_stream))
+                if evs is not None:
+                    evs[1].record(stream)
+            rounds = max(0, (max(n, 1) - 1).bit_length() - 11)
+            launches_per_step = 1 + 2 * rounds
+            units = n
+
+        for _ in range(args.warmup):
+            step()
+        stream.synchronize()
+        barrier(dist_on)
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            t0.record(stream)
+            for i in range(args.steps):
+                step(evs[i])
+                launches += launches_per_step
+            t1.record(stream)
+            stream.synchronize()
+        torch.cuda.synchronize()
+        barrier(dist_on)
+        ms = t0.elapsed_time(t1)
+        kern_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in evs)
+    ms = max_over_ranks(ms, dist_on)
+    ms_per_step = ms / args.steps
+    value = units * ws * args.steps / (ms / 1e3)
+
+    if cfg["kind"] == "merge":
+        alg_bytes = n * cfg["bytes_per"]  # read A+B once, write S once
+        kname = "merge_tiles_kernel (K2)"
+    else:
+        alg_bytes = n * 8 * (1 + max(0, (n - 1).bit_length() - 11))
+        kname = "mp_sort: block_sort + 19 x (round_partition + merge_tiles)"
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tpath = ROOT / "profiles" / f"traffic_config{args.config}.json"
+    if tpath.exists():
+        traffic = json.loads(tpath.read_text()).get("dram_bytes_per_launch")
+    result = {
+        "metric": "merged elements/s" if cfg["kind"] == "merge" else "merge-sort keys/s",
+        "value": value,
+        "unit": "elements/s" if cfg["kind"] == "merge" else "keys/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": key,
+        "data": "synthetic: SplitMix64 counter generator x_i=mix64(seed+i*0x9E3779B97F4A7C15), "
+                "sorted ascending before timing",
+        "config": {"workload": cfg["desc"], "l2": "inputs+output larger than L2 "
+                   "(no flush needed)" if alg_bytes > 4 * 126e6 else "fits in L2 (warm)",
+                   "parallelism": f"dp{ws}" if ws > 1 else "single GPU",
+                   "elements_per_gpu": units},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": kern_ms},
+    }
+    result["clocks"] = clk.summary()
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, cfg, torch, N, dev, local, dist_on, ws)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(cfg, a if cfg["kind"] == "merge" else data0,
+                                              b if cfg["kind"] == "merge" else None,
+                                              out if cfg["kind"] == "merge" else None, args)
+    return result
+
+
+def run_e2e(args, cfg, torch, N, dev, local, dist_on, ws):
+    """The same metric through the public host-buffer C ABI entry point
+    (mp_merge_host / mp_sort_host): pinned host inputs in, host output back,
+    all copies inside the timed region (wall clock around the synchronous
+    calls)."""
+    import numpy as np
+    key, kt = cfg["key"], KT[cfg["key"]]
+    steps = max(1, min(args.steps, args.e2e_steps))
+    with torch.cuda.device(dev):
+        if cfg["kind"] == "merge":
+            a, b, av, bv = make_inputs(torch, N, cfg, dev, torch.cuda.current_stream())
+            ha = a.cpu().pin_memory()
+            hb = b.cpu().pin_memory()
+            n = a.numel() + b.numel()
+            hout = torch.empty(n, dtype=a.dtype).pin_memory()
+            hav = hbv = houtv = None
+            if av is not None:
+                hav, hbv = av.cpu().pin_memory(), bv.cpu().pin_memory()
+                houtv = torch.empty(n, dtype=torch.uint32).pin_memory()
+            del a, b, av, bv
+            torch.cuda.synchronize()
+            p = (lambda t: t.data_ptr() if t is not None else None)
+
+            def call():
+                N.check(N.lib.mp_merge_host(kt, ha.data_ptr(), p(hav), ha.numel(), hb.data_ptr(),
+                                            p(hbv), hb.numel(), hout.data_ptr(), p(houtv), local))
+            h2d = (ha.numel() + hb.numel()) * KSIZE[key] + (n * 4 if hav is not None else 0)
+            d2h = n * KSIZE[key] + (n * 4 if hav is not None else 0)
+        else:
+            x = make_inputs(torch, N, cfg, dev, torch.cuda.current_stream())
+            hx = x.cpu().pin_memory()
+            hout = torch.empty_like(hx).pin_memory()
+            n = x.numel()
+            del x
+
+            def call():
+                N.check(N.lib.mp_sort_host(kt, hx.data_ptr(), None, n, hout.data_ptr(), None, local))
+            h2d = d2h = n * KSIZE[key]
+        for _ in range(min(2, args.warmup)):
+            call()
+        barrier(dist_on)
+        t = time.perf_counter()
+        for _ in range(steps):
+            call()
+        el = time.perf_counter() - t
+        barrier(dist_on)
+    el = max_over_ranks(el, dist_on)
+    unit = "elements/s" if cfg["kind"] == "merge" else "keys/s"
+    del np
+    return {"value": n * ws * steps / el, "unit": unit, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps,
+            "api": "mp_merge_host" if cfg["kind"] == "merge" else "mp_sort_host"}
+
+
+# --------------------------------------------------------------------------
+# reference (CPU) arm and cpu_baseline
+# --------------------------------------------------------------------------
+def ref_inputs_from_device(cfg, a, b):
+    """Host copies of the same input bytes the GPU arm uses."""
+    import numpy as np
+    if cfg["kind"] == "sort":
+        return a.cpu().numpy(), None
+    ha, hb = a.cpu().numpy(), b.cpu().numpy()
+    if cfg.get("vals"):
+        from oracle.bindings import KV_DTYPE
+        ka = np.zeros(len(ha), dtype=KV_DTYPE)
+        ka["key"], ka["val"] = ha, np.arange(len(ha), dtype=np.uint32)
+        kb = np.zeros(len(hb), dtype=KV_DTYPE)
+        kb["key"], kb["val"] = hb, np.arange(len(hb), dtype=np.uint32) | np.uint32(1 << 31)
+        return ka, kb
+    return ha, hb
+
+
+def host_inputs(cfg):
+    """Generate the config's inputs on the host with the C restatement's
+    generator (used when no GPU ran first, i.e. --impl reference)."""
+    import numpy as np
+    from oracle import bindings as B
+    P = B.port()
+    if cfg["kind"] == "sort":
+        return P.generate(cfg["gen"][0], 4, 0, cfg["n"]), None
+    a = P.radix_sort(P.generate(cfg["gen"][0], 1, 0, cfg["na"]))
+    b = P.radix_sort(P.generate(cfg["gen"][1], 2, 0, cfg["nb"]))
+    if cfg.get("vals"):
+        from oracle.bindings import KV_DTYPE
+        ka = np.zeros(len(a), dtype=KV_DTYPE)
+        ka["key"], ka["val"] = a, np.arange(len(a), dtype=np.uint32)
+        kb = np.zeros(len(b), dtype=KV_DTYPE)
+        kb["key"], kb["val"] = b, np.arange(len(b), dtype=np.uint32) | np.uint32(1 << 31)
+        return ka, kb
+    return a, b
+
+
+def time_reference(cfg, ha, hb, reps, budget_s, sample_frac=None):
+    """Time the reference's own CPU path: parallel_merge_into with a warm
+    thread_team(p = host cores) (parallel.hpp:151-162), or
+    parallel_merge_sort(span, p) (sort.hpp:132-148).  Returns
+    (elements per second, seconds per rep, p, sample description, out)."""
+    from oracle import bindings as B
+    R = B.ref()
+    p = B.host_cores()
+    S = "kv" if cfg.get("vals") else cfg["key"]
+    if cfg["kind"] == "merge":
+        import numpy as np
+        team = R.team(p)
+        out = np.empty(len(ha) + len(hb), dtype=B.DTYPES[S])
+        for _ in range(2):  # warm the team
+            R.merge(S, ha, hb, team=team, out=out)
+        times = []
+        t_start = time.perf_counter()
+        for _ in range(reps):
+            t = time.perf_counter()
+            R.merge(S, ha, hb, team=team, out=out)
+            times.append(time.perf_counter() - t)
+            if time.perf_counter() - t_start > budget_s:
+                break
+        team.close()
+        sec = statistics.median(times)
+        n = len(ha) + len(hb)
+        sample = (f"full config input ({n} elements), parallel_merge_into with a warm "
+                  f"thread_team({p}), median of {len(times)} reps")
+        return n / sec, sec, p, sample, out
+    # sort: a bounded prefix of the same keys (full 2^30 takes ~40 s on 8 threads)
+    n = len(ha)
+    m = n if sample_frac is None else max(1 << 20, int(n * sample_frac))
+    d = ha[:m]
+    times = []
+    for _ in range(max(1, reps)):
+        t = time.perf_counter()
+        out, _ = R.merge_sort(S, d, p=p)
+        times.append(time.perf_counter() - t)
+        if sum(times) > budget_s:
+            break
+    sec = statistics.median(times)
+    sample = (f"first {m} of the {n} config keys, parallel_merge_sort(span, p={p}) incl. its "
+              f"copy/alloc, median of {len(times)} reps")
+    return m / sec, sec, p, sample, out
+
+
+def cpu_baseline(cfg, a, b, out_dev, args):
+    from oracle import bindings as B
+    if not B.REF_LIB.exists():
+        return {"value": None, "unit": None, "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    ha, hb = ref_inputs_from_device(cfg, a, b)
+    frac = None if cfg["kind"] == "merge" else 1 / 16
+    val, sec, p, sample, out = time_reference(cfg, ha, hb, reps=5, budget_s=20, sample_frac=frac)
+    res = {"value": val, "unit": "elements/s" if cfg["kind"] == "merge" else "keys/s",
+           "cores": p, "kind": "reference", "sample": sample, "seconds_per_rep": sec}
+    if out_dev is not None:  # verify before report (mergebench.cpp:263-265)
+        got = out_dev.cpu().numpy()
+        want = out["key"] if cfg.get("vals") else out
+        res["gpu_output_bit_exact_vs_reference"] = bool(got.tobytes() == want.tobytes())
+    return res
+
+
+def run_reference(args, cfg, ws, rank):
+    """--impl reference: the reference's own CPU implementation on this box's
+    host cores, same config/metric/unit; each step = one full merge (or a
+    bounded sort sample)."""
+    if rank != 0:
+        return None
+    from oracle import bindings as B
+    if not B.REF_LIB.exists():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libmergepath_ref.so not built"}
+    ha, hb = host_inputs(cfg)
+    S = "kv" if cfg.get("vals") else cfg["key"]
+    R = B.ref()
+    p = B.host_cores()
+    times = []
+    if cfg["kind"] == "merge":
+        import numpy as np
+        team = R.team(p)
+        out = np.empty(len(ha) + len(hb), dtype=B.DTYPES[S])
+        for _ in range(args.warmup):
+            R.merge(S, ha, hb, team=team, out=out)
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            R.merge(S, ha, hb, team=team, out=out)
+            times.append(time.perf_counter() - t)
+        team.close()
+        units = len(ha) + len(hb)
+        sample = (f"full config input per step ({units} elements), parallel_merge_into, "
+                  f"warm thread_team({p})")
+    else:
+        m = max(1 << 20, len(ha) // 64)
+        d = ha[:m]
+        for _ in range(min(args.warmup, 1)):
+            R.merge_sort(S, d, p=p)
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            R.merge_sort(S, d, p=p)
+            times.append(time.perf_counter() - t)
+        units = m
+        sample = f"first {m} config keys per step, parallel_merge_sort(span, p={p})"
+    total = sum(times)
+    value = units * len(times) / total
+    unit = "elements/s" if cfg["kind"] == "merge" else "keys/s"
+    return {
+        "impl": "reference",
+        "metric": "merged elements/s" if cfg["kind"] == "merge" else "merge-sort keys/s",
+        "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / len(times) * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg["key"], "data": "synthetic (same generator)",
+        "config": {"workload": cfg["desc"], "parallelism": f"cpu threads {p}"},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": p, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# --------------------------------------------------------------------------
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[1])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    ws, rank, local = dist_env()
+    dist_on = ws > 1
+    if args.impl == "reference":
+        res = run_reference(args, cfg, ws, rank)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return 0
+    if dist_on:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if dist_on and cfg["kind"] == "merge":
+        from paper_1406_2628_b200.multigpu import bench_distributed
+        res = bench_distributed(args, cfg, ws, rank, local)
+    else:
+        res = run_ours(args, cfg, ws, rank, local, dist_on)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if dist_on:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

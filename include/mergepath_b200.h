@@ -1,0 +1,143 @@
+/*
+ * mergepath_b200.h -- C ABI of the B200-native Merge Path library
+ * (libmergepath_b200.so, built from paper_1406_2628_b200/csrc/).
+ *
+ * This is the drop-in boundary.  The reference exposes its hot path as C++
+ * templates over <T, Comp> (no compiled ABI at all):
+ *   diagonal_search / partition          core.hpp:120-146
+ *   sequential_merge                     core.hpp:148-180
+ *   parallel_merge[_into]                parallel.hpp:151-179
+ *   segmented_parallel_merge[_into]      parallel.hpp:200-236
+ *   plan_segments                        parallel.hpp:258-292
+ *   parallel_merge_checksum / segmented_parallel_merge_checksum
+ *                                        parallel.hpp:181-198, :238-256
+ *   parallel_merge_sort                  sort.hpp:132-148
+ *   cache_efficient_parallel_sort        sort.hpp:150-195
+ * The drop-in C++ headers in include/mergepath/ keep those exact template
+ * signatures and forward every supported (T, Comp) pair to the entry points
+ * below; INTEGRATION.md shows the binding.  Plain pointers and sizes only.
+ *
+ * Conventions
+ *   - Device entry points (no suffix) take DEVICE pointers and a
+ *     cudaStream_t passed as void*; they are asynchronous on that stream.
+ *   - *_host entry points take HOST pointers (pageable or pinned), stage
+ *     through the GPU `device` and return when the result is in host memory.
+ *   - Every call returns an mp_status; mp_last_error() describes the last
+ *     failure on the calling thread.
+ *   - Ties: equal keys take A first (core.hpp:79-87), so merges are stable
+ *     with A as the left operand and sorts are stable w.r.t. input index.
+ *   - Optional uint32 values travel with their keys (SoA records ordered by
+ *     key only).  Pass NULL for keys-only.  MP_KEY_ELEMENT keys carry their
+ *     own tag and take no separate values.
+ */
+#ifndef MERGEPATH_B200_H
+#define MERGEPATH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mp_key_type {
+  MP_KEY_U32 = 0,     /* std::less<uint32_t> */
+  MP_KEY_I32 = 1,     /* std::less<int32_t> */
+  MP_KEY_F32 = 2,     /* IEEE 754 totalOrder on float32 (-0.0 < +0.0) */
+  MP_KEY_U64 = 3,     /* std::less<uint64_t> */
+  MP_KEY_I64 = 4,     /* std::less<int64_t> */
+  MP_KEY_ELEMENT = 5  /* reference `element` {int64 key; uint32 tag}, 16 B,
+                         ordered by key only (core.hpp:39-53) */
+} mp_key_type;
+
+typedef enum mp_status {
+  MP_OK = 0,
+  MP_ERR_INVALID = 1,     /* std::invalid_argument in the reference */
+  MP_ERR_CUDA = 2,        /* CUDA launch / runtime failure */
+  MP_ERR_OOM = 3,         /* device or pinned allocation failed */
+  MP_ERR_UNSUPPORTED = 4  /* key type / value combination not supported */
+} mp_status;
+
+/* Message for the last non-OK status on this thread ("" if none). */
+const char *mp_last_error(void);
+/* ABI version (major*100 + minor). */
+int mp_abi_version(void);
+/* Size in bytes of one key of `key_type` (0 if unknown). */
+uint64_t mp_key_size(int key_type);
+
+/* ---- partition (core.hpp:120-146) ------------------------------------- */
+/* a_offs[i] = a_off of the merge path on diagonal floor(i*(na+nb)/p),
+ * i = 0..p (p+1 device uint64 entries); b_off = diagonal - a_off.
+ * p == 0 -> MP_ERR_INVALID (core.hpp:139-140).  `comparisons` (device
+ * uint64, may be NULL) accumulates the element comparisons of the p+1
+ * searches exactly as the reference counts them (core.hpp:120-132). */
+int mp_partition(int key_type, const void *a, uint64_t na, const void *b,
+                 uint64_t nb, uint64_t p, uint64_t *a_offs,
+                 uint64_t *comparisons, void *stream);
+
+/* a_offs[k] = a_off on diagonal diags[k] (clamped to na+nb), k < count.
+ * `comparisons` as for mp_partition. */
+int mp_diagonal_search(int key_type, const void *a, uint64_t na,
+                       const void *b, uint64_t nb, const uint64_t *diags,
+                       uint64_t count, uint64_t *a_offs,
+                       uint64_t *comparisons, void *stream);
+
+/* ---- merge (parallel.hpp:151-179, :200-236) --------------------------- */
+/* out[0, na+nb) = stable merge of A and B.  Values optional (all three of
+ * a_vals/b_vals/out_vals, or none).  Output must not overlap the inputs. */
+int mp_merge(int key_type, const void *a, const uint32_t *a_vals, uint64_t na,
+             const void *b, const uint32_t *b_vals, uint64_t nb, void *out,
+             uint32_t *out_vals, void *stream);
+
+/* The same merge in two stream-ordered phases over a caller-owned device
+ * workspace (for CUDA graphs, overlap and per-kernel timing):
+ *   mp_merge_plan    -- K1: tile split points into `workspace`
+ *   mp_merge_execute -- K2: the tile merge reading those split points
+ * mp_merge == plan + execute.  The workspace depends only on the key type
+ * and na + nb. */
+uint64_t mp_merge_workspace_bytes(int key_type, uint64_t na, uint64_t nb);
+int mp_merge_plan(int key_type, const void *a, uint64_t na, const void *b,
+                  uint64_t nb, void *workspace, void *stream);
+int mp_merge_execute(int key_type, const void *a, const uint32_t *a_vals,
+                     uint64_t na, const void *b, const uint32_t *b_vals,
+                     uint64_t nb, void *out, uint32_t *out_vals,
+                     const void *workspace, void *stream);
+
+/* Register-sink merge (parallel.hpp:181-198): *sum (device uint64) =
+ * sum over merged positions i of (i+1)*mix64(key_i) (core.hpp:200-245),
+ * without writing the merged array.  Integer key types and ELEMENT;
+ * F32 keys are bit-cast. */
+int mp_merge_checksum(int key_type, const void *a, uint64_t na, const void *b,
+                      uint64_t nb, uint64_t *sum, void *stream);
+
+/* ---- sort (sort.hpp:132-195) ------------------------------------------ */
+/* Stable sort of keys[0,n) in place (vals optional, permuted alongside).
+ * scratch may be NULL (stream-ordered pool allocation) or a device buffer of
+ * at least mp_sort_scratch_bytes() bytes. */
+uint64_t mp_sort_scratch_bytes(int key_type, int with_vals, uint64_t n);
+int mp_sort(int key_type, void *keys, uint32_t *vals, uint64_t n,
+            void *scratch, uint64_t scratch_bytes, void *stream);
+
+/* ---- host-buffer entry points (synchronous) --------------------------- */
+int mp_partition_host(int key_type, const void *a, uint64_t na, const void *b,
+                      uint64_t nb, uint64_t p, uint64_t *a_offs, int device);
+int mp_merge_host(int key_type, const void *a, const uint32_t *a_vals,
+                  uint64_t na, const void *b, const uint32_t *b_vals,
+                  uint64_t nb, void *out, uint32_t *out_vals, int device);
+int mp_sort_host(int key_type, const void *keys, const uint32_t *vals,
+                 uint64_t n, void *out_keys, uint32_t *out_vals, int device);
+int mp_merge_checksum_host(int key_type, const void *a, uint64_t na,
+                           const void *b, uint64_t nb, uint64_t *sum,
+                           int device);
+
+/* ---- synthetic inputs (bench/tests; SURVEY.md §8d generator) ---------- */
+/* out[k] = config key kind `gen_kind` at global index first+k for `seed`:
+ * 0 u32 = x>>32; 1 i32 in [0,1024) = x>>54; 2 u64 = x; 3 u64 < 2^40;
+ * 4 u64 in [2^40, 2^64).  x_i = mix64(seed + i*0x9E3779B97F4A7C15). */
+int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,
+                void *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MERGEPATH_B200_H */

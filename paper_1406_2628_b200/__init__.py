@@ -1,0 +1,17 @@
+"""paper_1406_2628_b200 -- B200-native Merge Path merge and merge sort.
+
+Hot path (BASELINE.json north_star): Merge Path partition -> merge and the
+bottom-up merge sort built on it, as hand-written sm_100a kernels behind the
+C ABI in include/mergepath_b200.h (libmergepath_b200.so, built in-tree).
+
+    from paper_1406_2628_b200 import mergepath as mp
+    out = mp.parallel_merge(a, b, p=8)        # a, b: sorted CUDA tensors
+    s = mp.parallel_merge_sort(keys, p=8)
+
+The multi-GPU layer (one process per GPU, torch.distributed) lives in
+paper_1406_2628_b200.multigpu.
+"""
+from . import _native  # noqa: F401  (fails loudly if the .so is missing)
+from . import mergepath  # noqa: F401
+
+__all__ = ["mergepath"]

@@ -1,0 +1,727 @@
+// mp_capi.cu -- the extern "C" boundary (include/mergepath_b200.h) and the
+// host-side launch logic for the Merge Path kernels.
+//
+// Every entry point validates its arguments the way the reference does
+// (invalid_argument conditions -> MP_ERR_INVALID), dispatches the key type to
+// a kernel template instantiation, launches on the caller's stream and maps
+// CUDA failures to status codes.  There is no CPU fallback: without a CUDA
+// device every call fails with MP_ERR_CUDA.
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/mergepath_b200.h"
+#include "mp_kernels.cuh"
+
+namespace {
+
+using namespace mpb;
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  return fail(e == cudaErrorMemoryAllocation ? MP_ERR_OOM : MP_ERR_CUDA,
+              "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define MP_CUDA(x)                                                             \
+  do {                                                                         \
+    const cudaError_t e_ = (x);                                                \
+    if (e_ != cudaSuccess)                                                     \
+      return cuda_fail(e_, #x);                                                \
+  } while (0)
+
+#define MP_LAUNCHED(what)                                                      \
+  do {                                                                         \
+    const cudaError_t e_ = cudaGetLastError();                                 \
+    if (e_ != cudaSuccess)                                                     \
+      return cuda_fail(e_, what);                                              \
+  } while (0)
+
+// Stream-ordered scratch from the device's default pool; the pool keeps its
+// memory (release threshold = max) so repeated calls do not hit the driver.
+void ensure_pool() {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
+    return;
+  std::call_once(once[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+struct ScratchGuard {  // frees a stream-ordered allocation on scope exit
+  void *p = nullptr;
+  cudaStream_t s = nullptr;
+  ~ScratchGuard() {
+    if (p)
+      cudaFreeAsync(p, s);
+  }
+};
+
+int alloc_scratch(ScratchGuard &g, size_t bytes, cudaStream_t s) {
+  ensure_pool();
+  g.s = s;
+  const cudaError_t e = cudaMallocAsync(&g.p, bytes ? bytes : 16, s);
+  if (e != cudaSuccess) {
+    g.p = nullptr;
+    return cuda_fail(e, "cudaMallocAsync(scratch)");
+  }
+  return MP_OK;
+}
+
+uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+template <class KT> bool aligned_keys(const void *p) {
+  return (reinterpret_cast<uintptr_t>(p) % alignof(typename KT::T)) == 0;
+}
+
+// ---- per-key-type tile shapes --------------------------------------------
+// Plain merge: odd VT (conflict-free staging, bulk-store epilogue).
+template <class KT> struct MergeCfg {
+  static constexpr int NT = 256;
+  static constexpr int VT = sizeof(typename KT::T) == 4   ? 15
+                            : sizeof(typename KT::T) == 8 ? 11
+                                                          : 7;
+};
+// Sort rounds: NV must divide 2 * 2048 (block-sort run length).
+template <class KT> struct SortMergeCfg {
+  static constexpr int NT = 256;
+  static constexpr int VT = sizeof(typename KT::T) == 4   ? 16
+                            : sizeof(typename KT::T) == 8 ? 8
+                                                          : 4;
+};
+constexpr int kBlockNT = 256;
+constexpr int kBlockVT = 8;
+constexpr uint64_t kRun = kBlockNT * kBlockVT;  // 2048-key block-sort runs
+
+template <class K> cudaError_t set_smem(K kernel, uint32_t bytes) {
+  if (bytes <= 48 * 1024)
+    return cudaSuccess;
+  return cudaFuncSetAttribute(kernel,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(bytes));
+}
+
+// ---- K1 -------------------------------------------------------------------
+template <class KT>
+int launch_partition(const void *a, uint64_t na, const void *b, uint64_t nb,
+                     uint64_t spacing, uint64_t p, uint64_t count,
+                     uint64_t *a_offs, cudaStream_t s,
+                     uint64_t *cmp = nullptr) {
+  using T = typename KT::T;
+  if (count == 0)
+    return MP_OK;
+  const unsigned blocks = static_cast<unsigned>(cdiv(count, 128));
+  partition_kernel<KT><<<blocks, 128, 0, s>>>(
+      static_cast<const T *>(a), na, static_cast<const T *>(b), nb, spacing, p,
+      count, a_offs, reinterpret_cast<unsigned long long *>(cmp));
+  MP_LAUNCHED("partition_kernel");
+  return MP_OK;
+}
+
+// ---- K1 + K2: plain merge --------------------------------------------------
+// Workspace of a plain merge = the tile partition array P[0..tiles].
+template <class KT> uint64_t merge_tiles(uint64_t n) {
+  constexpr uint64_t NV = MergeCfg<KT>::NT * MergeCfg<KT>::VT;
+  return cdiv(n, NV);
+}
+template <class KT> uint64_t merge_ws_bytes(uint64_t n) {
+  return n ? (merge_tiles<KT>(n) + 1) * sizeof(uint64_t) : 0;
+}
+
+// K1 at tile spacing: P[t] = a_off on diagonal t*NV.
+template <class KT>
+int merge_plan(const void *a, uint64_t na, const void *b, uint64_t nb,
+               uint64_t *P, cudaStream_t s) {
+  constexpr uint64_t NV = MergeCfg<KT>::NT * MergeCfg<KT>::VT;
+  const uint64_t n = na + nb;
+  if (n == 0)
+    return MP_OK;
+  if (merge_tiles<KT>(n) >= (1ull << 31))
+    return fail(MP_ERR_INVALID, "merge too large (%llu elements)",
+                (unsigned long long)n);
+  return launch_partition<KT>(a, na, b, nb, NV, 0, merge_tiles<KT>(n) + 1, P,
+                              s);
+}
+
+// K2 over the tiles planned by merge_plan.
+template <class KT, bool VALS, bool SINK>
+int merge_exec(const void *a, const uint32_t *av, uint64_t na, const void *b,
+               const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
+               unsigned long long *sum, const uint64_t *P, cudaStream_t s) {
+  using T = typename KT::T;
+  constexpr int NT = MergeCfg<KT>::NT, VT = MergeCfg<KT>::VT;
+  constexpr uint32_t NV = NT * VT;
+  const uint64_t n = na + nb;
+  if (n == 0)
+    return MP_OK;
+  const uint64_t tiles = merge_tiles<KT>(n);
+  constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
+  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, PlainMap, SINK>;
+  MP_CUDA(set_smem(kern, smem));
+  kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
+      PlainMap{P, n, NV}, static_cast<const T *>(a), av,
+      static_cast<const T *>(b), bv, static_cast<T *>(out), outv, sum);
+  MP_LAUNCHED("merge_tiles_kernel");
+  return MP_OK;
+}
+
+template <class KT, bool VALS, bool SINK>
+int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
+               const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
+               unsigned long long *sum, cudaStream_t s) {
+  const uint64_t n = na + nb;
+  if (n == 0)
+    return MP_OK;
+  ScratchGuard P;
+  if (int rc = alloc_scratch(P, merge_ws_bytes<KT>(n), s))
+    return rc;
+  uint64_t *Pp = static_cast<uint64_t *>(P.p);
+  if (int rc = merge_plan<KT>(a, na, b, nb, Pp, s))
+    return rc;
+  return merge_exec<KT, VALS, SINK>(a, av, na, b, bv, nb, out, outv, sum, Pp,
+                                    s);
+}
+
+// ---- K3 + (K4 + K2) x rounds: bottom-up merge sort ---------------------------
+struct SortLayout {
+  uint64_t keys_off, vals_off, part_off, total;
+};
+
+template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
+  using T = typename KT::T;
+  constexpr uint64_t NV = SortMergeCfg<KT>::NT * SortMergeCfg<KT>::VT;
+  auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  SortLayout L;
+  L.keys_off = 0;
+  L.vals_off = up(n * sizeof(T));
+  L.part_off = L.vals_off + (vals ? up(n * 4) : 0);
+  L.total = L.part_off + up((cdiv(n, NV) + 1) * sizeof(uint64_t));
+  return L;
+}
+
+template <class KT, bool VALS>
+int sort_impl(void *keys_, uint32_t *vals, uint64_t n, void *scratch,
+              uint64_t scratch_bytes, cudaStream_t s) {
+  using T = typename KT::T;
+  T *keys = static_cast<T *>(keys_);
+  if (n <= 1)
+    return MP_OK;
+  const SortLayout L = sort_layout<KT>(VALS, n);
+  ScratchGuard own;
+  char *ws = static_cast<char *>(scratch);
+  if (!ws) {
+    if (int rc = alloc_scratch(own, L.total, s))
+      return rc;
+    ws = static_cast<char *>(own.p);
+  } else if (scratch_bytes < L.total) {
+    return fail(MP_ERR_INVALID, "scratch too small: %llu < %llu bytes",
+                (unsigned long long)scratch_bytes,
+                (unsigned long long)L.total);
+  }
+  T *aux = reinterpret_cast<T *>(ws + L.keys_off);
+  uint32_t *auxv = VALS ? reinterpret_cast<uint32_t *>(ws + L.vals_off) : nullptr;
+  uint64_t *P = reinterpret_cast<uint64_t *>(ws + L.part_off);
+
+  int rounds = 0;
+  for (uint64_t w = kRun; w < n; w *= 2)
+    ++rounds;
+  // Block sort lands where an even/odd number of ping-pong rounds ends in
+  // `keys` (the result always lands back in the caller's buffer).
+  const bool in_place = (rounds % 2) == 0;
+  T *src = in_place ? keys : aux;
+  uint32_t *srcv = in_place ? vals : auxv;
+  T *dst = in_place ? aux : keys;
+  uint32_t *dstv = in_place ? auxv : vals;
+
+  {
+    constexpr uint32_t smem = block_sort_smem_bytes<KT, VALS, kBlockNT, kBlockVT>();
+    auto kern = block_sort_kernel<KT, VALS, kBlockNT, kBlockVT>;
+    MP_CUDA(set_smem(kern, smem));
+    kern<<<static_cast<unsigned>(cdiv(n, kRun)), kBlockNT, smem, s>>>(
+        keys, vals, src, srcv, n);
+    MP_LAUNCHED("block_sort_kernel");
+  }
+
+  constexpr int NT = SortMergeCfg<KT>::NT, VT = SortMergeCfg<KT>::VT;
+  constexpr uint32_t NV = NT * VT;
+  const uint64_t tiles = cdiv(n, NV);
+  constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
+  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, RoundMap, false>;
+  MP_CUDA(set_smem(kern, smem));
+  for (uint64_t w = kRun; w < n; w *= 2) {
+    round_partition_kernel<KT>
+        <<<static_cast<unsigned>(cdiv(tiles, 128)), 128, 0, s>>>(src, n, w, NV,
+                                                                 tiles, P);
+    MP_LAUNCHED("round_partition_kernel");
+    kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
+        RoundMap{P, n, w, NV}, src, srcv, src, srcv, dst, dstv, nullptr);
+    MP_LAUNCHED("merge_tiles_kernel(round)");
+    T *t = src;
+    src = dst;
+    dst = t;
+    uint32_t *tv = srcv;
+    srcv = dstv;
+    dstv = tv;
+  }
+  return MP_OK;
+}
+
+// ---- generators -------------------------------------------------------------
+__global__ void generate_kernel(int kind, uint64_t seed, uint64_t first,
+                                uint64_t n, void *out) {
+  const uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (k >= n)
+    return;
+  const uint64_t x = mix64_dev(seed + (first + k) * 0x9E3779B97F4A7C15ULL);
+  switch (kind) {
+  case 0:
+    static_cast<uint32_t *>(out)[k] = static_cast<uint32_t>(x >> 32);
+    break;
+  case 1:
+    static_cast<int32_t *>(out)[k] = static_cast<int32_t>(x >> 54);
+    break;
+  case 2:
+    static_cast<unsigned long long *>(out)[k] = x;
+    break;
+  case 3:
+    static_cast<unsigned long long *>(out)[k] = x >> 24;
+    break;
+  case 4:
+    static_cast<unsigned long long *>(out)[k] =
+        (1ull << 40) + __umul64hi(x, ~0ull - (1ull << 40) + 1ull);
+    break;
+  }
+}
+
+// ---- dispatch --------------------------------------------------------------
+template <template <class> class F, class... Args>
+int dispatch(int kt, Args &&...args) {
+  switch (kt) {
+  case kU32:
+    return F<KeyU32>::run(args...);
+  case kI32:
+    return F<KeyI32>::run(args...);
+  case kF32:
+    return F<KeyF32>::run(args...);
+  case kU64:
+    return F<KeyU64>::run(args...);
+  case kI64:
+    return F<KeyI64>::run(args...);
+  case kElement:
+    return F<KeyElement>::run(args...);
+  default:
+    return fail(MP_ERR_UNSUPPORTED, "unknown key type %d", kt);
+  }
+}
+
+template <class KT> struct PartitionOp {
+  static int run(const void *a, uint64_t na, const void *b, uint64_t nb,
+                 uint64_t p, uint64_t *a_offs, uint64_t *cmp, cudaStream_t s) {
+    if (!aligned_keys<KT>(a) || !aligned_keys<KT>(b))
+      return fail(MP_ERR_INVALID, "misaligned key pointer");
+    return launch_partition<KT>(a, na, b, nb, 0, p, p + 1, a_offs, s, cmp);
+  }
+};
+
+template <class KT> struct DiagonalsOp {
+  static int run(const void *a, uint64_t na, const void *b, uint64_t nb,
+                 const uint64_t *diags, uint64_t count, uint64_t *a_offs,
+                 uint64_t *cmp, cudaStream_t s) {
+    using T = typename KT::T;
+    if (count == 0)
+      return MP_OK;
+    diagonals_kernel<KT><<<static_cast<unsigned>(cdiv(count, 128)), 128, 0, s>>>(
+        static_cast<const T *>(a), na, static_cast<const T *>(b), nb, diags,
+        count, a_offs, reinterpret_cast<unsigned long long *>(cmp));
+    MP_LAUNCHED("diagonals_kernel");
+    return MP_OK;
+  }
+};
+
+// phase 0: plan + execute with a pool workspace; 1: plan into ws;
+// 2: execute with a planned ws.
+template <class KT> struct MergeOp {
+  static int run(const void *a, const uint32_t *av, uint64_t na, const void *b,
+                 const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
+                 int phase, uint64_t *ws, cudaStream_t s) {
+    if (!aligned_keys<KT>(a) || !aligned_keys<KT>(b) ||
+        (phase != 1 && !aligned_keys<KT>(out)))
+      return fail(MP_ERR_INVALID, "misaligned key pointer");
+    if (phase == 1)
+      return merge_plan<KT>(a, na, b, nb, ws, s);
+    const bool vals = av || bv || outv;
+    if (vals) {
+      if (KT::kind == kElement)
+        return fail(MP_ERR_UNSUPPORTED, "ELEMENT keys carry their own tag");
+      if (!outv || (na && !av) || (nb && !bv))
+        return fail(MP_ERR_INVALID, "values must be given for A, B and out");
+      if (phase == 2)
+        return merge_exec<KT, true, false>(a, av, na, b, bv, nb, out, outv,
+                                           nullptr, ws, s);
+      return merge_impl<KT, true, false>(a, av, na, b, bv, nb, out, outv,
+                                         nullptr, s);
+    }
+    if (phase == 2)
+      return merge_exec<KT, false, false>(a, nullptr, na, b, nullptr, nb, out,
+                                          nullptr, nullptr, ws, s);
+    return merge_impl<KT, false, false>(a, nullptr, na, b, nullptr, nb, out,
+                                        nullptr, nullptr, s);
+  }
+};
+
+template <class KT> struct MergeWsOp {
+  static int run(uint64_t n, uint64_t *out) {
+    *out = merge_ws_bytes<KT>(n);
+    return MP_OK;
+  }
+};
+
+template <class KT> struct ChecksumOp {
+  static int run(const void *a, uint64_t na, const void *b, uint64_t nb,
+                 uint64_t *sum, cudaStream_t s) {
+    if (!aligned_keys<KT>(a) || !aligned_keys<KT>(b))
+      return fail(MP_ERR_INVALID, "misaligned key pointer");
+    MP_CUDA(cudaMemsetAsync(sum, 0, sizeof(uint64_t), s));
+    return merge_impl<KT, false, true>(
+        a, nullptr, na, b, nullptr, nb, nullptr, nullptr,
+        reinterpret_cast<unsigned long long *>(sum), s);
+  }
+};
+
+template <class KT> struct SortOp {
+  static int run(void *keys, uint32_t *vals, uint64_t n, void *scratch,
+                 uint64_t scratch_bytes, cudaStream_t s) {
+    if (!aligned_keys<KT>(keys))
+      return fail(MP_ERR_INVALID, "misaligned key pointer");
+    if (vals) {
+      if (KT::kind == kElement)
+        return fail(MP_ERR_UNSUPPORTED, "ELEMENT keys carry their own tag");
+      return sort_impl<KT, true>(keys, vals, n, scratch, scratch_bytes, s);
+    }
+    return sort_impl<KT, false>(keys, nullptr, n, scratch, scratch_bytes, s);
+  }
+};
+
+template <class KT> struct ScratchOp {
+  static int run(bool vals, uint64_t n, uint64_t *out) {
+    *out = n <= 1 ? 0 : sort_layout<KT>(vals, n).total;
+    return MP_OK;
+  }
+};
+
+uint64_t key_size(int kt) {
+  switch (kt) {
+  case kU32:
+  case kI32:
+  case kF32:
+    return 4;
+  case kU64:
+  case kI64:
+    return 8;
+  case kElement:
+    return 16;
+  default:
+    return 0;
+  }
+}
+
+// Host staging: one cached non-blocking stream per device.
+cudaStream_t host_stream(int device) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64)
+    return nullptr;
+  if (!streams[device])
+    cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+  return streams[device];
+}
+
+struct DeviceScope {  // restores the caller's current device
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    err = cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    if (prev >= 0)
+      cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char *mp_last_error(void) { return g_err.c_str(); }
+int mp_abi_version(void) { return 100; }
+uint64_t mp_key_size(int key_type) { return key_size(key_type); }
+
+int mp_partition(int kt, const void *a, uint64_t na, const void *b,
+                 uint64_t nb, uint64_t p, uint64_t *a_offs,
+                 uint64_t *comparisons, void *stream) {
+  g_err.clear();
+  if (p == 0)
+    return fail(MP_ERR_INVALID, "partition: p must be positive");
+  if (!a_offs)
+    return fail(MP_ERR_INVALID, "partition: a_offs is NULL");
+  return dispatch<PartitionOp>(kt, a, na, b, nb, p, a_offs, comparisons,
+                               static_cast<cudaStream_t>(stream));
+}
+
+int mp_diagonal_search(int kt, const void *a, uint64_t na, const void *b,
+                       uint64_t nb, const uint64_t *diags, uint64_t count,
+                       uint64_t *a_offs, uint64_t *comparisons, void *stream) {
+  g_err.clear();
+  if (count && (!diags || !a_offs))
+    return fail(MP_ERR_INVALID, "diagonal_search: NULL array");
+  return dispatch<DiagonalsOp>(kt, a, na, b, nb, diags, count, a_offs,
+                               comparisons, static_cast<cudaStream_t>(stream));
+}
+
+int mp_merge(int kt, const void *a, const uint32_t *a_vals, uint64_t na,
+             const void *b, const uint32_t *b_vals, uint64_t nb, void *out,
+             uint32_t *out_vals, void *stream) {
+  g_err.clear();
+  if ((na && !a) || (nb && !b) || ((na + nb) && !out))
+    return fail(MP_ERR_INVALID, "merge: NULL array");
+  return dispatch<MergeOp>(kt, a, a_vals, na, b, b_vals, nb, out, out_vals, 0,
+                           static_cast<uint64_t *>(nullptr),
+                           static_cast<cudaStream_t>(stream));
+}
+
+uint64_t mp_merge_workspace_bytes(int kt, uint64_t na, uint64_t nb) {
+  uint64_t out = 0;
+  if (dispatch<MergeWsOp>(kt, na + nb, &out) != MP_OK)
+    return 0;
+  return out;
+}
+
+int mp_merge_plan(int kt, const void *a, uint64_t na, const void *b,
+                  uint64_t nb, void *workspace, void *stream) {
+  g_err.clear();
+  if ((na && !a) || (nb && !b) || ((na + nb) && !workspace))
+    return fail(MP_ERR_INVALID, "merge_plan: NULL array");
+  return dispatch<MergeOp>(kt, a, static_cast<const uint32_t *>(nullptr), na,
+                           b, static_cast<const uint32_t *>(nullptr), nb,
+                           static_cast<void *>(nullptr),
+                           static_cast<uint32_t *>(nullptr), 1,
+                           static_cast<uint64_t *>(workspace),
+                           static_cast<cudaStream_t>(stream));
+}
+
+int mp_merge_execute(int kt, const void *a, const uint32_t *a_vals,
+                     uint64_t na, const void *b, const uint32_t *b_vals,
+                     uint64_t nb, void *out, uint32_t *out_vals,
+                     const void *workspace, void *stream) {
+  g_err.clear();
+  if ((na && !a) || (nb && !b) || ((na + nb) && (!out || !workspace)))
+    return fail(MP_ERR_INVALID, "merge_execute: NULL array");
+  return dispatch<MergeOp>(kt, a, a_vals, na, b, b_vals, nb, out, out_vals, 2,
+                           const_cast<uint64_t *>(
+                               static_cast<const uint64_t *>(workspace)),
+                           static_cast<cudaStream_t>(stream));
+}
+
+int mp_merge_checksum(int kt, const void *a, uint64_t na, const void *b,
+                      uint64_t nb, uint64_t *sum, void *stream) {
+  g_err.clear();
+  if ((na && !a) || (nb && !b) || !sum)
+    return fail(MP_ERR_INVALID, "merge_checksum: NULL array");
+  return dispatch<ChecksumOp>(kt, a, na, b, nb, sum,
+                              static_cast<cudaStream_t>(stream));
+}
+
+uint64_t mp_sort_scratch_bytes(int kt, int with_vals, uint64_t n) {
+  uint64_t out = 0;
+  if (dispatch<ScratchOp>(kt, with_vals != 0, n, &out) != MP_OK)
+    return 0;
+  return out;
+}
+
+int mp_sort(int kt, void *keys, uint32_t *vals, uint64_t n, void *scratch,
+            uint64_t scratch_bytes, void *stream) {
+  g_err.clear();
+  if (n && !keys)
+    return fail(MP_ERR_INVALID, "sort: NULL keys");
+  return dispatch<SortOp>(kt, keys, vals, n, scratch, scratch_bytes,
+                          static_cast<cudaStream_t>(stream));
+}
+
+int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,
+                void *out, void *stream) {
+  g_err.clear();
+  if (gen_kind < 0 || gen_kind > 4)
+    return fail(MP_ERR_INVALID, "generate: unknown kind %d", gen_kind);
+  if (n == 0)
+    return MP_OK;
+  generate_kernel<<<static_cast<unsigned>(cdiv(n, 256)), 256, 0,
+                    static_cast<cudaStream_t>(stream)>>>(gen_kind, seed, first,
+                                                          n, out);
+  MP_LAUNCHED("generate_kernel");
+  return MP_OK;
+}
+
+// ---- host-buffer entry points ----------------------------------------------
+int mp_partition_host(int kt, const void *a, uint64_t na, const void *b,
+                      uint64_t nb, uint64_t p, uint64_t *a_offs, int device) {
+  g_err.clear();
+  const uint64_t ks = key_size(kt);
+  if (!ks)
+    return fail(MP_ERR_UNSUPPORTED, "unknown key type %d", kt);
+  if (p == 0)
+    return fail(MP_ERR_INVALID, "partition: p must be positive");
+  DeviceScope ds(device);
+  if (ds.err != cudaSuccess)
+    return cuda_fail(ds.err, "cudaSetDevice");
+  cudaStream_t s = host_stream(device);
+  ScratchGuard g;
+  const uint64_t ab = (na * ks + 255) & ~uint64_t(255);
+  const uint64_t bb = (nb * ks + 255) & ~uint64_t(255);
+  if (int rc = alloc_scratch(g, ab + bb + (p + 1) * 8, s))
+    return rc;
+  char *d = static_cast<char *>(g.p);
+  if (na)
+    MP_CUDA(cudaMemcpyAsync(d, a, na * ks, cudaMemcpyHostToDevice, s));
+  if (nb)
+    MP_CUDA(cudaMemcpyAsync(d + ab, b, nb * ks, cudaMemcpyHostToDevice, s));
+  uint64_t *offs = reinterpret_cast<uint64_t *>(d + ab + bb);
+  if (int rc = mp_partition(kt, d, na, d + ab, nb, p, offs, nullptr, s))
+    return rc;
+  MP_CUDA(cudaMemcpyAsync(a_offs, offs, (p + 1) * 8, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  return MP_OK;
+}
+
+int mp_merge_host(int kt, const void *a, const uint32_t *av, uint64_t na,
+                  const void *b, const uint32_t *bv, uint64_t nb, void *out,
+                  uint32_t *outv, int device) {
+  g_err.clear();
+  const uint64_t ks = key_size(kt);
+  if (!ks)
+    return fail(MP_ERR_UNSUPPORTED, "unknown key type %d", kt);
+  const uint64_t n = na + nb;
+  if (n == 0)
+    return MP_OK;
+  if ((na && !a) || (nb && !b) || !out)
+    return fail(MP_ERR_INVALID, "merge: NULL array");
+  const bool vals = av || bv || outv;
+  if (vals && (!outv || (na && !av) || (nb && !bv)))
+    return fail(MP_ERR_INVALID, "values must be given for A, B and out");
+  DeviceScope ds(device);
+  if (ds.err != cudaSuccess)
+    return cuda_fail(ds.err, "cudaSetDevice");
+  cudaStream_t s = host_stream(device);
+  auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  const uint64_t o_a = 0, o_b = up(na * ks), o_o = o_b + up(nb * ks);
+  const uint64_t o_av = o_o + up(n * ks), o_bv = o_av + (vals ? up(na * 4) : 0);
+  const uint64_t o_ov = o_bv + (vals ? up(nb * 4) : 0);
+  const uint64_t total = o_ov + (vals ? up(n * 4) : 0);
+  ScratchGuard g;
+  if (int rc = alloc_scratch(g, total, s))
+    return rc;
+  char *d = static_cast<char *>(g.p);
+  if (na)
+    MP_CUDA(cudaMemcpyAsync(d + o_a, a, na * ks, cudaMemcpyHostToDevice, s));
+  if (nb)
+    MP_CUDA(cudaMemcpyAsync(d + o_b, b, nb * ks, cudaMemcpyHostToDevice, s));
+  if (vals && na)
+    MP_CUDA(cudaMemcpyAsync(d + o_av, av, na * 4, cudaMemcpyHostToDevice, s));
+  if (vals && nb)
+    MP_CUDA(cudaMemcpyAsync(d + o_bv, bv, nb * 4, cudaMemcpyHostToDevice, s));
+  int rc = mp_merge(kt, d + o_a, vals ? reinterpret_cast<uint32_t *>(d + o_av) : nullptr,
+                    na, d + o_b, vals ? reinterpret_cast<uint32_t *>(d + o_bv) : nullptr,
+                    nb, d + o_o, vals ? reinterpret_cast<uint32_t *>(d + o_ov) : nullptr, s);
+  if (rc)
+    return rc;
+  MP_CUDA(cudaMemcpyAsync(out, d + o_o, n * ks, cudaMemcpyDeviceToHost, s));
+  if (vals)
+    MP_CUDA(cudaMemcpyAsync(outv, d + o_ov, n * 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  return MP_OK;
+}
+
+int mp_merge_checksum_host(int kt, const void *a, uint64_t na, const void *b,
+                           uint64_t nb, uint64_t *sum, int device) {
+  g_err.clear();
+  const uint64_t ks = key_size(kt);
+  if (!ks)
+    return fail(MP_ERR_UNSUPPORTED, "unknown key type %d", kt);
+  if (!sum)
+    return fail(MP_ERR_INVALID, "merge_checksum: NULL sum");
+  DeviceScope ds(device);
+  if (ds.err != cudaSuccess)
+    return cuda_fail(ds.err, "cudaSetDevice");
+  cudaStream_t s = host_stream(device);
+  const uint64_t ab = (na * ks + 255) & ~uint64_t(255);
+  const uint64_t bb = (nb * ks + 255) & ~uint64_t(255);
+  ScratchGuard g;
+  if (int rc = alloc_scratch(g, ab + bb + 256, s))
+    return rc;
+  char *d = static_cast<char *>(g.p);
+  if (na)
+    MP_CUDA(cudaMemcpyAsync(d, a, na * ks, cudaMemcpyHostToDevice, s));
+  if (nb)
+    MP_CUDA(cudaMemcpyAsync(d + ab, b, nb * ks, cudaMemcpyHostToDevice, s));
+  uint64_t *dsum = reinterpret_cast<uint64_t *>(d + ab + bb);
+  if (int rc = mp_merge_checksum(kt, d, na, d + ab, nb, dsum, s))
+    return rc;
+  MP_CUDA(cudaMemcpyAsync(sum, dsum, 8, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  return MP_OK;
+}
+
+int mp_sort_host(int kt, const void *keys, const uint32_t *vals, uint64_t n,
+                 void *out_keys, uint32_t *out_vals, int device) {
+  g_err.clear();
+  const uint64_t ks = key_size(kt);
+  if (!ks)
+    return fail(MP_ERR_UNSUPPORTED, "unknown key type %d", kt);
+  if (n == 0)
+    return MP_OK;
+  if (!keys || !out_keys || (vals && !out_vals))
+    return fail(MP_ERR_INVALID, "sort: NULL array");
+  DeviceScope ds(device);
+  if (ds.err != cudaSuccess)
+    return cuda_fail(ds.err, "cudaSetDevice");
+  cudaStream_t s = host_stream(device);
+  const uint64_t kb = (n * ks + 255) & ~uint64_t(255);
+  const uint64_t vb = vals ? ((n * 4 + 255) & ~uint64_t(255)) : 0;
+  ScratchGuard g;
+  if (int rc = alloc_scratch(g, kb + vb, s))
+    return rc;
+  char *d = static_cast<char *>(g.p);
+  MP_CUDA(cudaMemcpyAsync(d, keys, n * ks, cudaMemcpyHostToDevice, s));
+  uint32_t *dv = vals ? reinterpret_cast<uint32_t *>(d + kb) : nullptr;
+  if (vals)
+    MP_CUDA(cudaMemcpyAsync(dv, vals, n * 4, cudaMemcpyHostToDevice, s));
+  if (int rc = mp_sort(kt, d, dv, n, nullptr, 0, s))
+    return rc;
+  MP_CUDA(cudaMemcpyAsync(out_keys, d, n * ks, cudaMemcpyDeviceToHost, s));
+  if (vals)
+    MP_CUDA(cudaMemcpyAsync(out_vals, dv, n * 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  return MP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,444 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Small cases: bit-exact against fixtures recorded from the reference itself
+(tests/golden/ref_fixtures.npz) and against the C restatement on the same
+seeded inputs.  Full BASELINE.json sizes: size-independent properties
+(sortedness, multiset equality, A-before-B on ties, each input appearing in
+order in the output) that together pin the unique stable merge.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import element_array, fixture_cases, same
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("u32", "i32", "f32", "u64", "i64", "el")
+TORCH_DT = {}
+
+
+def _torch():
+    import torch
+    global TORCH_DT
+    TORCH_DT = {"u32": torch.uint32, "i32": torch.int32, "f32": torch.float32,
+                "u64": torch.uint64, "i64": torch.int64}
+    return torch
+
+
+def to_dev(x, S, dev):
+    torch = _torch()
+    if S == "el":
+        return torch.from_numpy(np.ascontiguousarray(x).view(np.int64).copy()).to(dev)
+    if S == "f32":
+        x = np.ascontiguousarray(x).view(np.float32)
+    return torch.from_numpy(np.ascontiguousarray(x).copy()).to(dev)
+
+
+def from_dev(t, S):
+    from oracle.bindings import ELEMENT_DTYPE
+    x = t.cpu().numpy()
+    if S == "el":
+        return x.view(ELEMENT_DTYPE)
+    if S == "f32":
+        return x.view(np.uint32)
+    return x
+
+
+def key_type(S):
+    from paper_1406_2628_b200 import _native as N
+    return {"u32": N.KEY_U32, "i32": N.KEY_I32, "f32": N.KEY_F32, "u64": N.KEY_U64,
+            "i64": N.KEY_I64, "el": N.KEY_ELEMENT}[S]
+
+
+# ------------------------------------------------------------ fixtures
+def test_fixture_merges_device(cuda, fixtures):
+    from paper_1406_2628_b200 import mergepath as mp
+    for S, ci in fixture_cases(fixtures, "m"):
+        if S not in KEYS:
+            continue
+        k = f"{S}/{ci}"
+        a, b = fixtures[k + "/a"], fixtures[k + "/b"]
+        out = mp.parallel_merge(to_dev(a, S, cuda), to_dev(b, S, cuda), 3, key_type=key_type(S))
+        assert same(from_dev(out, S), fixtures[k + "/merged"]), k
+
+
+def test_fixture_merges_host_entry(cuda, fixtures):
+    from paper_1406_2628_b200 import mergepath as mp
+    for S, ci in fixture_cases(fixtures, "m"):
+        if S not in KEYS:
+            continue
+        k = f"{S}/{ci}"
+        a, b = fixtures[k + "/a"], fixtures[k + "/b"]
+        out = mp.parallel_merge(a, b, 8, key_type=key_type(S))
+        assert same(out, fixtures[k + "/merged"]), k
+
+
+def test_fixture_kv_merge_with_values(cuda, fixtures):
+    torch = _torch()
+    from paper_1406_2628_b200 import mergepath as mp
+    for S, ci in fixture_cases(fixtures, "m"):
+        if S != "kv":
+            continue
+        k = f"kv/{ci}"
+        a, b, want = fixtures[k + "/a"], fixtures[k + "/b"], fixtures[k + "/merged"]
+        ak = torch.from_numpy(a["key"].copy()).to(cuda)
+        bk = torch.from_numpy(b["key"].copy()).to(cuda)
+        av = torch.from_numpy(a["val"].copy()).to(cuda)
+        bv = torch.from_numpy(b["val"].copy()).to(cuda)
+        out, outv = mp.parallel_merge(ak, bk, 8, a_vals=av, b_vals=bv)
+        assert out.cpu().numpy().tolist() == want["key"].tolist(), k
+        assert outv.cpu().numpy().tolist() == want["val"].tolist(), k
+
+
+def test_fixture_partitions_and_stats(cuda, fixtures):
+    from paper_1406_2628_b200 import mergepath as mp
+    for S, ci in fixture_cases(fixtures, "m"):
+        if S not in KEYS:
+            continue
+        k = f"{S}/{ci}"
+        a, b = to_dev(fixtures[k + "/a"], S, cuda), to_dev(fixtures[k + "/b"], S, cuda)
+        kt = key_type(S)
+        for p in (1, 3, 8):
+            ref = fixtures[k + f"/part{p}"]
+            cnt = [0]
+            pts = mp.partition(a, b, p, comparisons=cnt, key_type=kt)
+            assert [x.a_off for x in pts] == ref[0].tolist(), (k, p)
+            assert [x.b_off for x in pts] == ref[1].tolist(), (k, p)
+            assert cnt[0] == int(ref[2][0]), (k, p)
+            st = mp.MergeStats()
+            mp.parallel_merge(a, b, p, stats=st, key_type=kt)
+            assert [st.partition_comparisons, st.merge_steps] == \
+                fixtures[k + f"/mergestats{p}"].tolist(), (k, p)
+        for p, C in ((3, 12), (8, 48), (1, 3)):
+            st = mp.MergeStats()
+            mp.segmented_parallel_merge(a, b, p, C, stats=st, key_type=kt)
+            wins = [[w.a_consumed, w.b_consumed] for w in st.windows]
+            assert wins == fixtures[k + f"/seg{p}_{C}"].tolist(), (k, p, C)
+            plan = mp.plan_segments(a, b, p, C, key_type=kt)
+            ref = fixtures[k + f"/plan{p}_{C}"].tolist()
+            assert [plan.window_len, plan.p_eff, plan.iterations] == ref[:3]
+            assert [[s.a_off, s.b_off] for s in plan.starting_points] == \
+                fixtures[k + f"/planstarts{p}_{C}"].tolist(), (k, p, C)
+
+
+def test_fixture_sorts(cuda, fixtures):
+    from paper_1406_2628_b200 import mergepath as mp
+    for S, ci in fixture_cases(fixtures, "s"):
+        k = f"{S}/{ci}"
+        d = fixtures[k + "/in"]
+        want = fixtures[k + "/sorted"]
+        if S == "kv":
+            torch = _torch()
+            keys = torch.from_numpy(d["key"].copy()).to(cuda)
+            vals = torch.from_numpy(d["val"].copy()).to(cuda)
+            out, outv = mp.parallel_merge_sort(keys, 3, vals=vals)
+            assert out.cpu().numpy().tolist() == want["key"].tolist(), k
+            assert outv.cpu().numpy().tolist() == want["val"].tolist(), k
+            continue
+        st = mp.SortStats()
+        out = mp.parallel_merge_sort(to_dev(d, S, cuda), 3, stats=st, key_type=key_type(S))
+        assert same(from_dev(out, S), want), k
+        assert st.merge_rounds == int(fixtures[k + "/rounds"][0])
+        out2 = mp.cache_efficient_parallel_sort(d, 4, 48, key_type=key_type(S))
+        assert same(out2, want), k
+
+
+def test_fixture_checksum(cuda, fixtures):
+    from paper_1406_2628_b200 import mergepath as mp
+    a, b = fixtures["checksum/a"], fixtures["checksum/b"]
+    want = fixtures["checksum/sum"].tolist()
+    assert mp.parallel_merge_checksum(a, b, 4, key_type=key_type("el")) == want[0]
+    assert mp.segmented_parallel_merge_checksum(to_dev(a, "el", cuda), to_dev(b, "el", cuda),
+                                                4, 48, key_type=key_type("el")) == want[1]
+
+
+# ------------------------------------------------------------ KATs on device
+def test_kats_on_device(cuda, kats):
+    from paper_1406_2628_b200 import mergepath as mp
+    kt = key_type("el")
+    for c in kats["diagonal_search"]:
+        a, b = element_array(c["a"]), element_array(c["b"])
+        cnt = [0]
+        pt = mp.diagonal_search(a, b, c["d"], comparisons=cnt, key_type=kt)
+        assert [pt.a_off, pt.b_off] == c["want"], c["src"]
+        if "comparisons" in c:
+            assert cnt[0] == c["comparisons"]
+    for c in kats["partition"]:
+        pts = mp.partition(element_array(c["a"]), element_array(c["b"]), c["p"], key_type=kt)
+        assert [[p.a_off, p.b_off] for p in pts] == c["want"], c["src"]
+    for c in kats["stable_merge"]:
+        a = element_array(c["a"], c["a_tag_base"])
+        b = element_array(c["b"], c["b_tag_base"])
+        lo, hi = c.get("p_range", [1, 1])
+        for p in range(lo, hi + 1):
+            out = mp.parallel_merge(a, b, p, key_type=kt)
+            assert out["tag"].tolist() == c["want_tags"], c["src"]
+    for c in kats["invalid_argument"]:
+        a = element_array([1, 2])
+        with pytest.raises(ValueError):
+            op = getattr(mp, c["op"])
+            if c["op"] in ("partition", "parallel_merge"):
+                op(a, a, c["p"], key_type=kt)
+            elif c["op"] in ("segmented_parallel_merge", "plan_segments"):
+                op(a, a, c["p"], c["C"], key_type=kt)
+            elif c["op"] == "parallel_merge_sort":
+                op(a, c["p"], key_type=kt)
+            else:
+                op(a, c["p"], c["C"], key_type=kt)
+
+
+# ------------------------------------------------------------ vs the C restatement
+SHAPES = [(0, 0), (0, 1), (1, 0), (1, 1), (3839, 1), (1, 3840), (3840, 3840), (3841, 3839),
+          (5000, 17), (17, 5000), (123457, 98765), (1 << 17, 1 << 17)]
+
+
+@pytest.mark.parametrize("S", KEYS)
+def test_random_merges_vs_oracle(cuda, port, S):
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(7)
+    for na, nb in SHAPES:
+        for dup in (4, 1 << 30):
+            a = _rand_sorted(S, rng, na, dup)
+            b = _rand_sorted(S, rng, nb, dup)
+            if S == "el":
+                b["tag"] += np.uint32(1 << 24)
+            want, _, _, _ = port.merge(S, a, b)
+            got = mp.parallel_merge(to_dev(a, S, cuda), to_dev(b, S, cuda), 8,
+                                    key_type=key_type(S))
+            assert same(from_dev(got, S), want), (S, na, nb, dup)
+
+
+@pytest.mark.parametrize("S", ("u32", "f32", "u64", "i64"))
+def test_random_merges_with_values_vs_oracle(cuda, port, S):
+    torch = _torch()
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(11)
+    for na, nb in SHAPES:
+        a = _rand_sorted(S, rng, na, 16)
+        b = _rand_sorted(S, rng, nb, 16)
+        av = np.arange(na, dtype=np.uint32)
+        bv = np.arange(nb, dtype=np.uint32) | np.uint32(1 << 31)
+        want, wantv, _, _ = port.merge(S, a, b, av=av, bv=bv)
+        got, gotv = mp.parallel_merge(to_dev(a, S, cuda), to_dev(b, S, cuda), 1,
+                                      a_vals=torch.from_numpy(av).to(cuda),
+                                      b_vals=torch.from_numpy(bv).to(cuda), key_type=key_type(S))
+        assert same(from_dev(got, S), want), (S, na, nb)
+        assert np.array_equal(gotv.cpu().numpy(), wantv), (S, na, nb)
+
+
+def test_unaligned_views_exercise_edge_copies(cuda, port):
+    """Sub-views at every 4-byte offset: the bulk-copy interior shrinks and
+    the head/tail copies by ordinary loads take over."""
+    torch = _torch()
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(3)
+    base_a = np.sort(rng.integers(0, 1000, 20000).astype(np.uint32))
+    base_b = np.sort(rng.integers(0, 1000, 20000).astype(np.uint32))
+    da, db = torch.from_numpy(base_a).to(cuda), torch.from_numpy(base_b).to(cuda)
+    for oa in range(4):
+        for ob in range(4):
+            for la, lb in ((19000, 17), (5, 7), (3, 0), (7777, 7779)):
+                a, b = base_a[oa:oa + la], base_b[ob:ob + lb]
+                want, _, _, _ = port.merge("u32", a, b)
+                out_full = torch.empty(la + lb + 3, dtype=torch.uint32, device=cuda)
+                out = out_full[(oa + ob) % 4:(oa + ob) % 4 + la + lb]
+                mp.parallel_merge_into(da[oa:oa + la], db[ob:ob + lb], out, 2)
+                assert np.array_equal(out.cpu().numpy(), want), (oa, ob, la, lb)
+
+
+@pytest.mark.parametrize("S", KEYS)
+def test_random_sorts_vs_oracle(cuda, port, S):
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(13)
+    for n in (0, 1, 2, 2047, 2048, 2049, 4095, 4096, 4097, 10001, 65537, 300000):
+        for dup in (3, 1 << 30):
+            d = _rand_unsorted(S, rng, n, dup)
+            want, _, _ = port.merge_sort(S, d)
+            got = mp.parallel_merge_sort(to_dev(d, S, cuda), 4, key_type=key_type(S))
+            assert same(from_dev(got, S), want), (S, n, dup)
+
+
+@pytest.mark.parametrize("S", ("u32", "i32", "f32", "u64", "i64"))
+def test_sort_with_values_is_stable(cuda, port, S):
+    torch = _torch()
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(17)
+    for n in (1, 100, 2048, 5000, 123456):
+        d = _rand_unsorted(S, rng, n, 7)
+        v = np.arange(n, dtype=np.uint32)
+        want, wantv, _ = port.merge_sort(S, d, vals=v)
+        got, gotv = mp.parallel_merge_sort(to_dev(d, S, cuda), 2,
+                                           vals=torch.from_numpy(v).to(cuda),
+                                           key_type=key_type(S))
+        assert same(from_dev(got, S), want) and np.array_equal(gotv.cpu().numpy(), wantv), (S, n)
+
+
+def test_checksum_vs_oracle(cuda, port):
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(19)
+    for S in ("u32", "i32", "u64", "i64", "el", "f32"):
+        for na, nb in ((0, 0), (10, 0), (1000, 2000), (70001, 50000)):
+            a, b = _rand_sorted(S, rng, na, 50), _rand_sorted(S, rng, nb, 50)
+            out, _, _, _ = port.merge(S, a, b)
+            want = port.checksum(S, out)
+            got = mp.parallel_merge_checksum(to_dev(a, S, cuda), to_dev(b, S, cuda), 4,
+                                             key_type=key_type(S))
+            assert got == want, (S, na, nb)
+
+
+def test_device_generator_matches_oracle(cuda, port):
+    torch = _torch()
+    from paper_1406_2628_b200 import _native as N
+    for kind, dt in ((0, torch.uint32), (1, torch.int32), (2, torch.uint64), (3, torch.uint64),
+                     (4, torch.uint64)):
+        out = torch.empty(100003, dtype=dt, device=cuda)
+        N.check(N.lib.mp_generate(kind, 9, 12345, out.numel(), out.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream))
+        assert np.array_equal(out.cpu().numpy(), port.generate(kind, 9, 12345, 100003)), kind
+
+
+# ------------------------------------------------------------ BASELINE configs
+def test_config1_bit_exact_and_partition(cuda, port):
+    """Config 1: u32 2^20 + 2^20, seeds 1/2, p = 8: bit-exact output and the
+    9 partition points equal the reference's partition(in, 8)."""
+    torch = _torch()
+    from oracle import bindings as B
+    from paper_1406_2628_b200 import mergepath as mp
+    a = port.radix_sort(port.generate(0, 1, 0, 1 << 20))
+    b = port.radix_sort(port.generate(0, 2, 0, 1 << 20))
+    if B.REF_LIB.exists():
+        R = B.ref()
+        want, _, _ = R.merge("u32", a, b, p=8)
+        oa, ob, _ = R.partition("u32", a, b, 8)
+    else:
+        want, _, _, _ = port.merge("u32", a, b, p=8)
+        oa, _ = port.partition("u32", a, b, 8)
+    da, db = torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda)
+    got = mp.parallel_merge(da, db, 8)
+    assert np.array_equal(got.cpu().numpy(), want)
+    pts = mp.partition(da, db, 8)
+    assert [p.a_off for p in pts] == oa.tolist()
+    assert mp.parallel_merge(a, b, 8).tobytes() == want.tobytes()  # host entry
+
+
+def _sorted_dev(kind, seed, n, dev):
+    torch = _torch()
+    from paper_1406_2628_b200 import _native as N
+    dt = {0: torch.uint32, 1: torch.int32, 2: torch.uint64, 3: torch.uint64, 4: torch.uint64}[kind]
+    x = torch.empty(n, dtype=dt, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    N.check(N.lib.mp_generate(kind, seed, 0, n, x.data_ptr(), st))
+    N.check(N.lib.mp_sort(N.KEY_U32 if kind == 0 else N.KEY_I32 if kind == 1 else N.KEY_U64,
+                          x.data_ptr(), None, n, None, 0, st))
+    return x
+
+
+def test_config2_full_size_properties(cuda):
+    """Config 2: i32 2^28 + 2^28 in [0,1024): sorted, and per-key counts of
+    the output equal the sum of the inputs' (multiset equality).  For bare
+    keys these two properties determine the merged bytes."""
+    torch = _torch()
+    from paper_1406_2628_b200 import mergepath as mp
+    n = 1 << 28
+    a = _sorted_dev(1, 1, n, cuda)
+    b = _sorted_dev(1, 2, n, cuda)
+    assert bool((a[1:] >= a[:-1]).all()) and bool((b[1:] >= b[:-1]).all())
+    out = mp.parallel_merge(a, b, 8)
+    assert bool((out[1:] >= out[:-1]).all())
+    ca = torch.bincount(a, minlength=1024)
+    cb = torch.bincount(b, minlength=1024)
+    co = torch.bincount(out, minlength=1024)
+    assert torch.equal(ca + cb, co)
+    del out
+    # the p-way partition points split the output at equal-size boundaries
+    pts = mp.partition(a, b, 8)
+    for i, p in enumerate(pts):
+        assert p.d == (i * 2 * n) // 8
+
+
+@pytest.mark.parametrize("variant", ["3a", "3b"])
+def test_config3_full_size_stability(cuda, variant):
+    """Config 3: u64 keys + u32 values (source index, bit 31 marks B),
+    |A| = 2^29, |B| = 2^25.  Properties that pin the unique stable merge:
+    keys sorted; A-origin values appear as 0,1,2,... and B-origin values as
+    0,1,2,... (each input in order); keys match their source; on equal keys
+    no B element precedes an A element."""
+    torch = _torch()
+    from paper_1406_2628_b200 import mergepath as mp
+    na, nb = 1 << 29, 1 << 25
+    if variant == "3a":
+        a = _sorted_dev(2, 1, na, cuda)
+        b = _sorted_dev(2, 2, nb, cuda)
+    else:
+        a = _sorted_dev(4, 1, na, cuda)
+        b = _sorted_dev(3, 2, nb, cuda)
+    av = torch.arange(na, dtype=torch.int32, device=cuda).view(torch.uint32)
+    # j | 0x80000000 as a bit pattern == j - 2^31 as int32
+    bv = (torch.arange(nb, dtype=torch.int32, device=cuda)
+          + torch.iinfo(torch.int32).min).view(torch.uint32)
+    out, outv = mp.parallel_merge(a, b, 8, a_vals=av, b_vals=bv)
+    del av, bv
+    ok = out.view(torch.int64)  # compare u64 through signed view with offset
+    s = (ok ^ torch.iinfo(torch.int64).min)
+    assert bool((s[1:] >= s[:-1]).all())
+    del s
+    v = outv.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    from_b = v >= (1 << 31)
+    ia = v[~from_b]
+    ib = v[from_b] - (1 << 31)
+    assert ia.numel() == na and ib.numel() == nb
+    assert torch.equal(ia, torch.arange(na, device=cuda))
+    assert torch.equal(ib, torch.arange(nb, device=cuda))
+    del ia, ib
+    # tie rule: equal adjacent keys never go B then A
+    eq = ok[1:] == ok[:-1]
+    assert not bool((eq & from_b[:-1] & ~from_b[1:]).any())
+    if variant == "3b":  # B entirely below A: output = B then A
+        assert bool(from_b[:nb].all()) and not bool(from_b[nb:].any())
+
+
+def test_config4_sort_full_size(cuda):
+    """Config 4 on one GPU: 2^30 u32 keys, 2048-key block sort + 19 rounds;
+    equals torch.sort of the same keys (bare keys: sorted order is unique)."""
+    torch = _torch()
+    from paper_1406_2628_b200 import _native as N
+    n = 1 << 30
+    x = torch.empty(n, dtype=torch.uint32, device=cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    N.check(N.lib.mp_generate(0, 4, 0, n, x.data_ptr(), st))
+    ref = torch.sort(x.view(torch.int32).to(torch.int64) & 0xFFFFFFFF).values
+    N.check(N.lib.mp_sort(N.KEY_U32, x.data_ptr(), None, n, None, 0, st))
+    got = x.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    assert torch.equal(got, ref)
+
+
+# ------------------------------------------------------------ helpers
+def _rand_sorted(S, rng, n, dup):
+    from oracle.bindings import ELEMENT_DTYPE
+    r = max(2, min(dup, 1 << 62))
+    if S == "el":
+        e = np.zeros(n, dtype=ELEMENT_DTYPE)
+        e["key"] = np.sort(rng.integers(-r, r, n))
+        e["tag"] = np.arange(n, dtype=np.uint32)
+        return e
+    if S == "f32":
+        x = (rng.integers(-r, r, n) / 7.0).astype(np.float32)
+        x[rng.random(n) < 0.05] = -0.0
+        u = x.view(np.uint32)
+        key = np.where(u & 0x80000000, ~u, u | 0x80000000)
+        return u[np.argsort(key, kind="stable")]
+    dt = {"u32": np.uint32, "i32": np.int32, "u64": np.uint64, "i64": np.int64}[S]
+    if np.dtype(dt).kind == "u":
+        return np.sort(rng.integers(0, min(r, np.iinfo(dt).max), n).astype(dt))
+    return np.sort(rng.integers(-min(r, np.iinfo(dt).max), min(r, np.iinfo(dt).max), n).astype(dt))
+
+
+def _rand_unsorted(S, rng, n, dup):
+    x = _rand_sorted(S, rng, n, dup)
+    perm = rng.permutation(n)
+    x = x[perm]
+    if S == "el":
+        x["tag"] = np.arange(n, dtype=np.uint32)
+    return x
