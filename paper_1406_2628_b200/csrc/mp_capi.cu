@@ -101,16 +101,23 @@ template <class KT> struct MergeCfg {
                             : sizeof(typename KT::T) == 8 ? 11
                                                           : 7;
 };
-// Sort rounds: NV must divide 2 * 2048 (block-sort run length).
+// Sort rounds: the tile (TILE outputs) must divide 2 * 2048 (block-sort run
+// length) so no tile straddles two run pairs.  TILE is a power of two, but
+// the thread shape keeps VT odd (conflict-free smem access, bulk-store
+// epilogue) with NT*VT >= TILE; surplus threads own empty diagonals.
 template <class KT> struct SortMergeCfg {
-  static constexpr int NT = 256;
-  static constexpr int VT = sizeof(typename KT::T) == 4   ? 16
-                            : sizeof(typename KT::T) == 8 ? 8
-                                                          : 4;
+  static constexpr int TILE = sizeof(typename KT::T) == 4   ? 4096
+                              : sizeof(typename KT::T) == 8 ? 2048
+                                                            : 1024;
+  static constexpr int VT = sizeof(typename KT::T) == 4   ? 15
+                            : sizeof(typename KT::T) == 8 ? 11
+                                                          : 7;
+  static constexpr int NT = ((TILE + VT - 1) / VT + 31) / 32 * 32;
 };
-constexpr int kBlockNT = 256;
-constexpr int kBlockVT = 8;
+constexpr int kBlockNT = 128;
+constexpr int kBlockVT = 16;
 constexpr uint64_t kRun = kBlockNT * kBlockVT;  // 2048-key block-sort runs
+static_assert(kRun == 2048, "round pshift assumes 2048-key runs");
 
 template <class K> cudaError_t set_smem(K kernel, uint32_t bytes) {
   if (bytes <= 48 * 1024)
@@ -208,7 +215,7 @@ struct SortLayout {
 
 template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
   using T = typename KT::T;
-  constexpr uint64_t NV = SortMergeCfg<KT>::NT * SortMergeCfg<KT>::VT;
+  constexpr uint64_t NV = SortMergeCfg<KT>::TILE;
   auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
   SortLayout L;
   L.keys_off = 0;
@@ -262,18 +269,21 @@ int sort_impl(void *keys_, uint32_t *vals, uint64_t n, void *scratch,
   }
 
   constexpr int NT = SortMergeCfg<KT>::NT, VT = SortMergeCfg<KT>::VT;
-  constexpr uint32_t NV = NT * VT;
+  constexpr uint32_t NV = SortMergeCfg<KT>::TILE;
+  static_assert(NT * VT >= int(NV) && (2 * kRun) % NV == 0, "round tile shape");
   const uint64_t tiles = cdiv(n, NV);
   constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
   auto kern = merge_tiles_kernel<KT, VALS, NT, VT, RoundMap, false>;
   MP_CUDA(set_smem(kern, smem));
-  for (uint64_t w = kRun; w < n; w *= 2) {
+  uint32_t pshift = 12;  // 2 * kRun == 1 << 12
+  for (uint64_t w = kRun; w < n; w *= 2, ++pshift) {
     round_partition_kernel<KT>
-        <<<static_cast<unsigned>(cdiv(tiles, 128)), 128, 0, s>>>(src, n, w, NV,
-                                                                 tiles, P);
+        <<<static_cast<unsigned>(cdiv(tiles, 128)), 128, 0, s>>>(
+            src, n, w, pshift, NV, tiles, P);
     MP_LAUNCHED("round_partition_kernel");
     kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
-        RoundMap{P, n, w, NV}, src, srcv, src, srcv, dst, dstv, nullptr);
+        RoundMap{P, n, w, NV, pshift}, src, srcv, src, srcv, dst, dstv,
+        nullptr);
     MP_LAUNCHED("merge_tiles_kernel(round)");
     T *t = src;
     src = dst;
@@ -469,6 +479,166 @@ struct DeviceScope {  // restores the caller's current device
   }
 };
 
+// ---------------------------------------------------------------------------
+// Host-buffer merge, pipelined over PCIe.
+//
+// The output is cut into chunks of Q elements at host-side Merge Path splits
+// (the same diagonal search, run on the host arrays: Theorem 14 makes every
+// chunk an independent merge).  Chunk k flows through a ring of kSlots
+// device slots on three streams:  H2D (copy engine 1) -> K1+K2 (SMs) ->
+// D2H (copy engine 2), so the inbound copy of chunk k+1, the merge of chunk
+// k and the outbound copy of chunk k-1 overlap.  The bound is
+// max(H2D bytes, D2H bytes) / PCIe bandwidth instead of their sum.
+// ---------------------------------------------------------------------------
+constexpr int kSlots = 3;
+
+struct HostPipe {
+  std::mutex mu;  // one host call per device at a time
+  bool init = false;
+  cudaStream_t h2d = nullptr, cmp = nullptr, d2h = nullptr;
+  cudaEvent_t ev_h2d[kSlots] = {}, ev_cmp[kSlots] = {}, ev_d2h[kSlots] = {};
+  void *buf = nullptr;
+  size_t buf_bytes = 0;
+
+  int setup() {
+    if (init)
+      return MP_OK;
+    MP_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    MP_CUDA(cudaStreamCreateWithFlags(&cmp, cudaStreamNonBlocking));
+    MP_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < kSlots; ++i) {
+      MP_CUDA(cudaEventCreateWithFlags(&ev_h2d[i], cudaEventDisableTiming));
+      MP_CUDA(cudaEventCreateWithFlags(&ev_cmp[i], cudaEventDisableTiming));
+      MP_CUDA(cudaEventCreateWithFlags(&ev_d2h[i], cudaEventDisableTiming));
+    }
+    init = true;
+    return MP_OK;
+  }
+  int reserve(size_t bytes) {
+    if (bytes <= buf_bytes)
+      return MP_OK;
+    if (buf) {
+      cudaFree(buf);
+      buf = nullptr;
+      buf_bytes = 0;
+    }
+    MP_CUDA(cudaMalloc(&buf, bytes));
+    buf_bytes = bytes;
+    return MP_OK;
+  }
+};
+
+HostPipe &host_pipe(int device) {
+  static HostPipe pipes[64];
+  return pipes[device & 63];
+}
+
+template <class KT>
+uint64_t host_diag_search(const typename KT::T *a, uint64_t na,
+                          const typename KT::T *b, uint64_t nb, uint64_t d) {
+  uint64_t lo = d > nb ? d - nb : 0;
+  uint64_t hi = d < na ? d : na;
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (KT::less(b[d - 1 - mid], a[mid]))  // core.hpp:110, ties to A
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+template <class KT, bool VALS>
+int merge_host_pipelined(const void *a_, const uint32_t *av, uint64_t na,
+                         const void *b_, const uint32_t *bv, uint64_t nb,
+                         void *out_, uint32_t *outv, int device) {
+  using T = typename KT::T;
+  constexpr uint64_t ks = sizeof(T);
+  const T *a = static_cast<const T *>(a_);
+  const T *b = static_cast<const T *>(b_);
+  T *out = static_cast<T *>(out_);
+  const uint64_t n = na + nb;
+  if (n == 0)
+    return MP_OK;
+  HostPipe &P = host_pipe(device);
+  std::lock_guard<std::mutex> lk(P.mu);
+  if (int rc = P.setup())
+    return rc;
+  // ~64 MiB of keys per chunk; never more chunks than needed
+  const uint64_t Q = std::max<uint64_t>(1, std::min<uint64_t>(n, (64ull << 20) / ks));
+  const uint64_t chunks = cdiv(n, Q);
+  auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  const uint64_t o_a = 0, o_b = up(Q * ks), o_o = o_b + up(Q * ks);
+  const uint64_t o_av = o_o + up(Q * ks);
+  const uint64_t o_bv = o_av + (VALS ? up(Q * 4) : 0);
+  const uint64_t o_ov = o_bv + (VALS ? up(Q * 4) : 0);
+  const uint64_t o_ws = o_ov + (VALS ? up(Q * 4) : 0);
+  const uint64_t slot_bytes = o_ws + up(merge_ws_bytes<KT>(Q));
+  if (int rc = P.reserve(slot_bytes * kSlots))
+    return rc;
+  uint64_t a_lo = 0;  // split of chunk k's start
+  for (uint64_t k = 0; k < chunks; ++k) {
+    const int s = static_cast<int>(k % kSlots);
+    char *base = static_cast<char *>(P.buf) + s * slot_bytes;
+    const uint64_t d0 = k * Q, d1 = std::min(n, d0 + Q);
+    const uint64_t a_hi = d1 == n ? na : host_diag_search<KT>(a, na, b, nb, d1);
+    const uint64_t ca = a_hi - a_lo, cb = (d1 - a_hi) - (d0 - a_lo);
+    const uint64_t b_lo = d0 - a_lo;
+    if (k >= kSlots)  // the slot's previous chunk has left the device
+      MP_CUDA(cudaStreamWaitEvent(P.h2d, P.ev_d2h[s], 0));
+    if (ca)
+      MP_CUDA(cudaMemcpyAsync(base + o_a, a + a_lo, ca * ks,
+                              cudaMemcpyHostToDevice, P.h2d));
+    if (cb)
+      MP_CUDA(cudaMemcpyAsync(base + o_b, b + b_lo, cb * ks,
+                              cudaMemcpyHostToDevice, P.h2d));
+    if (VALS && ca)
+      MP_CUDA(cudaMemcpyAsync(base + o_av, av + a_lo, ca * 4,
+                              cudaMemcpyHostToDevice, P.h2d));
+    if (VALS && cb)
+      MP_CUDA(cudaMemcpyAsync(base + o_bv, bv + b_lo, cb * 4,
+                              cudaMemcpyHostToDevice, P.h2d));
+    MP_CUDA(cudaEventRecord(P.ev_h2d[s], P.h2d));
+    MP_CUDA(cudaStreamWaitEvent(P.cmp, P.ev_h2d[s], 0));
+    uint64_t *ws = reinterpret_cast<uint64_t *>(base + o_ws);
+    if (int rc = merge_plan<KT>(base + o_a, ca, base + o_b, cb, ws, P.cmp))
+      return rc;
+    if (int rc = merge_exec<KT, VALS, false>(
+            base + o_a, VALS ? reinterpret_cast<uint32_t *>(base + o_av) : nullptr,
+            ca, base + o_b,
+            VALS ? reinterpret_cast<uint32_t *>(base + o_bv) : nullptr, cb,
+            base + o_o, VALS ? reinterpret_cast<uint32_t *>(base + o_ov) : nullptr,
+            nullptr, ws, P.cmp))
+      return rc;
+    MP_CUDA(cudaEventRecord(P.ev_cmp[s], P.cmp));
+    MP_CUDA(cudaStreamWaitEvent(P.d2h, P.ev_cmp[s], 0));
+    MP_CUDA(cudaMemcpyAsync(out + d0, base + o_o, (d1 - d0) * ks,
+                            cudaMemcpyDeviceToHost, P.d2h));
+    if (VALS)
+      MP_CUDA(cudaMemcpyAsync(outv + d0, base + o_ov, (d1 - d0) * 4,
+                              cudaMemcpyDeviceToHost, P.d2h));
+    MP_CUDA(cudaEventRecord(P.ev_d2h[s], P.d2h));
+    a_lo = a_hi;
+  }
+  MP_CUDA(cudaStreamSynchronize(P.d2h));
+  return MP_OK;
+}
+
+template <class KT> struct MergeHostOp {
+  static int run(const void *a, const uint32_t *av, uint64_t na, const void *b,
+                 const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
+                 int device) {
+    if (av || bv || outv) {
+      if (KT::kind == kElement)
+        return fail(MP_ERR_UNSUPPORTED, "ELEMENT keys carry their own tag");
+      return merge_host_pipelined<KT, true>(a, av, na, b, bv, nb, out, outv,
+                                            device);
+    }
+    return merge_host_pipelined<KT, false>(a, nullptr, na, b, nullptr, nb, out,
+                                           nullptr, device);
+  }
+};
+
 }  // namespace
 
 extern "C" {
@@ -631,34 +801,7 @@ int mp_merge_host(int kt, const void *a, const uint32_t *av, uint64_t na,
   DeviceScope ds(device);
   if (ds.err != cudaSuccess)
     return cuda_fail(ds.err, "cudaSetDevice");
-  cudaStream_t s = host_stream(device);
-  auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
-  const uint64_t o_a = 0, o_b = up(na * ks), o_o = o_b + up(nb * ks);
-  const uint64_t o_av = o_o + up(n * ks), o_bv = o_av + (vals ? up(na * 4) : 0);
-  const uint64_t o_ov = o_bv + (vals ? up(nb * 4) : 0);
-  const uint64_t total = o_ov + (vals ? up(n * 4) : 0);
-  ScratchGuard g;
-  if (int rc = alloc_scratch(g, total, s))
-    return rc;
-  char *d = static_cast<char *>(g.p);
-  if (na)
-    MP_CUDA(cudaMemcpyAsync(d + o_a, a, na * ks, cudaMemcpyHostToDevice, s));
-  if (nb)
-    MP_CUDA(cudaMemcpyAsync(d + o_b, b, nb * ks, cudaMemcpyHostToDevice, s));
-  if (vals && na)
-    MP_CUDA(cudaMemcpyAsync(d + o_av, av, na * 4, cudaMemcpyHostToDevice, s));
-  if (vals && nb)
-    MP_CUDA(cudaMemcpyAsync(d + o_bv, bv, nb * 4, cudaMemcpyHostToDevice, s));
-  int rc = mp_merge(kt, d + o_a, vals ? reinterpret_cast<uint32_t *>(d + o_av) : nullptr,
-                    na, d + o_b, vals ? reinterpret_cast<uint32_t *>(d + o_bv) : nullptr,
-                    nb, d + o_o, vals ? reinterpret_cast<uint32_t *>(d + o_ov) : nullptr, s);
-  if (rc)
-    return rc;
-  MP_CUDA(cudaMemcpyAsync(out, d + o_o, n * ks, cudaMemcpyDeviceToHost, s));
-  if (vals)
-    MP_CUDA(cudaMemcpyAsync(outv, d + o_ov, n * 4, cudaMemcpyDeviceToHost, s));
-  MP_CUDA(cudaStreamSynchronize(s));
-  return MP_OK;
+  return dispatch<MergeHostOp>(kt, a, av, na, b, bv, nb, out, outv, device);
 }
 
 int mp_merge_checksum_host(int kt, const void *a, uint64_t na, const void *b,

@@ -41,43 +41,43 @@ __host__ __device__ __forceinline__ uint32_t f32_order(uint32_t u) {
 struct KeyU32 {
   using T = uint32_t;
   static constexpr int kind = kU32;
-  __device__ __forceinline__ static bool less(T x, T y) { return x < y; }
-  __device__ __forceinline__ static T max_key() { return 0xFFFFFFFFu; }
+  __host__ __device__ __forceinline__ static bool less(T x, T y) { return x < y; }
+  __host__ __device__ __forceinline__ static T max_key() { return 0xFFFFFFFFu; }
 };
 struct KeyI32 {
   using T = int32_t;
   static constexpr int kind = kI32;
-  __device__ __forceinline__ static bool less(T x, T y) { return x < y; }
-  __device__ __forceinline__ static T max_key() { return 0x7FFFFFFF; }
+  __host__ __device__ __forceinline__ static bool less(T x, T y) { return x < y; }
+  __host__ __device__ __forceinline__ static T max_key() { return 0x7FFFFFFF; }
 };
 struct KeyF32 {  // keys stored as their raw uint32 bit patterns
   using T = uint32_t;
   static constexpr int kind = kF32;
-  __device__ __forceinline__ static bool less(T x, T y) {
+  __host__ __device__ __forceinline__ static bool less(T x, T y) {
     return f32_order(x) < f32_order(y);
   }
   // f32_order(0x7FFFFFFF) == 0xFFFFFFFF: the largest key in totalOrder.
-  __device__ __forceinline__ static T max_key() { return 0x7FFFFFFFu; }
+  __host__ __device__ __forceinline__ static T max_key() { return 0x7FFFFFFFu; }
 };
 struct KeyU64 {
   using T = unsigned long long;
   static constexpr int kind = kU64;
-  __device__ __forceinline__ static bool less(T x, T y) { return x < y; }
-  __device__ __forceinline__ static T max_key() { return ~0ULL; }
+  __host__ __device__ __forceinline__ static bool less(T x, T y) { return x < y; }
+  __host__ __device__ __forceinline__ static T max_key() { return ~0ULL; }
 };
 struct KeyI64 {
   using T = long long;
   static constexpr int kind = kI64;
-  __device__ __forceinline__ static bool less(T x, T y) { return x < y; }
-  __device__ __forceinline__ static T max_key() { return 0x7FFFFFFFFFFFFFFFLL; }
+  __host__ __device__ __forceinline__ static bool less(T x, T y) { return x < y; }
+  __host__ __device__ __forceinline__ static T max_key() { return 0x7FFFFFFFFFFFFFFFLL; }
 };
 struct KeyElement {
   using T = Element;
   static constexpr int kind = kElement;
-  __device__ __forceinline__ static bool less(const T &x, const T &y) {
+  __host__ __device__ __forceinline__ static bool less(const T &x, const T &y) {
     return x.key < y.key;
   }
-  __device__ __forceinline__ static T max_key() {
+  __host__ __device__ __forceinline__ static T max_key() {
     T e;
     e.key = 0x7FFFFFFFFFFFFFFFLL;
     e.tag = 0xFFFFFFFFu;

@@ -129,11 +129,12 @@ struct PlainMap {
 struct RoundMap {
   const uint64_t *P;
   uint64_t n;
-  uint64_t width;
+  uint64_t width;  // a power of two: 2 * width == 1 << pshift
   uint32_t nv;
+  uint32_t pshift;
   __device__ __forceinline__ TileWin window(uint64_t t) const {
     const uint64_t d0 = t * nv;
-    const uint64_t s = (d0 / (2 * width)) * (2 * width);
+    const uint64_t s = (d0 >> pshift) << pshift;
     const uint64_t la = (n - s) < width ? (n - s) : width;
     const uint64_t rest = n - s - la;
     const uint64_t lb = rest < width ? rest : width;
@@ -155,13 +156,14 @@ struct RoundMap {
 template <class KT>
 __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
                                        uint64_t n, uint64_t width,
-                                       uint32_t nv, uint64_t tiles,
+                                       uint32_t pshift, uint32_t nv,
+                                       uint64_t tiles,
                                        uint64_t *__restrict__ P) {
   const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (t >= tiles)
     return;
   const uint64_t d0 = t * nv;
-  const uint64_t s = (d0 / (2 * width)) * (2 * width);
+  const uint64_t s = (d0 >> pshift) << pshift;
   const uint64_t la = (n - s) < width ? (n - s) : width;
   const uint64_t rest = n - s - la;
   const uint64_t lb = rest < width ? rest : width;
@@ -198,25 +200,49 @@ __host__ __device__ constexpr uint32_t merge_smem_bytes() {
   return 16 + (in_bytes > st_bytes ? in_bytes : st_bytes);
 }
 
+// smem byte offset of the 16 B-aligned slot that mirrors global address g:
+// offset congruent to g (mod 16) so the bulk-copy interior is aligned.
+__device__ __forceinline__ uint32_t mirror_off(uint32_t at, const void *g) {
+  return ((at + 15u) & ~15u) + static_cast<uint32_t>(reinterpret_cast<uintptr_t>(g) & 15u);
+}
+
+// Stage `bytes` of global memory at g into smem[off, off+bytes): the aligned
+// interior through the bulk-copy engine (issued by thread 0, completes on
+// bar), the unaligned head and tail (< 16 B each) with ordinary loads.
+// Called by one warp (lane = 0..31): the head [0, lo) and tail [hi, bytes)
+// outside the 16 B-aligned interior are < 32 B in total.
+template <int ES>
+__device__ __forceinline__ void stage_edges(char *smem, uint32_t off,
+                                            const char *g, uint32_t bytes,
+                                            int lane) {
+  using W = typename std::conditional<
+      ES == 4, uint32_t,
+      typename std::conditional<ES == 8, unsigned long long, int4>::type>::type;
+  const uintptr_t s = reinterpret_cast<uintptr_t>(g);
+  const uintptr_t is = (s + 15) & ~uintptr_t(15);
+  const uintptr_t ie = (s + bytes) & ~uintptr_t(15);
+  const uint32_t lo = ie > is ? static_cast<uint32_t>(is - s) : bytes;
+  const uint32_t hi = ie > is ? static_cast<uint32_t>(ie - s) : bytes;
+  const uint32_t nh = lo / ES, nt = (bytes - hi) / ES;
+  const uint32_t l = static_cast<uint32_t>(lane);
+  if (l < nh + nt) {
+    const uint32_t o = l < nh ? l * ES : hi + (l - nh) * ES;
+    *reinterpret_cast<W *>(smem + off + o) = __ldg(reinterpret_cast<const W *>(g + o));
+  }
+}
+
 __device__ __forceinline__ char *align16p(char *p) {
   return reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(p) + 15) &
                                   ~uintptr_t(15));
 }
 
-// Copy the unaligned head [0, lo) and tail [hi, bytes) of a staged range
-// with ordinary loads, ES bytes at a time (ES divides 16 and the range).
-template <int ES, int NT>
-__device__ __forceinline__ void copy_edges(const ByteRange &r, uint32_t lo,
-                                           uint32_t hi) {
-  using W = typename std::conditional<
-      ES == 4, uint32_t,
-      typename std::conditional<ES == 8, unsigned long long, int4>::type>::type;
-  for (uint32_t o = threadIdx.x * ES; o < lo; o += NT * ES)
-    *reinterpret_cast<W *>(r.dst + o) =
-        __ldg(reinterpret_cast<const W *>(r.src + o));
-  for (uint32_t o = hi + threadIdx.x * ES; o < r.bytes; o += NT * ES)
-    *reinterpret_cast<W *>(r.dst + o) =
-        __ldg(reinterpret_cast<const W *>(r.src + o));
+__device__ __forceinline__ uint32_t interior_bytes(const char *g, uint32_t bytes,
+                                                   uint32_t *lo_out) {
+  const uintptr_t s = reinterpret_cast<uintptr_t>(g);
+  const uintptr_t is = (s + 15) & ~uintptr_t(15);
+  const uintptr_t ie = (s + bytes) & ~uintptr_t(15);
+  *lo_out = static_cast<uint32_t>(is - s);
+  return ie > is ? static_cast<uint32_t>(ie - is) : 0u;
 }
 
 // Checksum sink support (core.hpp:200-245): key_of is static_cast<uint64_t>
@@ -239,6 +265,11 @@ __device__ __forceinline__ uint64_t key_of(const Element &x) {
   return static_cast<uint64_t>(x.key);
 }
 
+template <class T>
+__device__ __forceinline__ T lds(const char *smem, uint32_t off) {
+  return *reinterpret_cast<const T *>(smem + off);
+}
+
 // SINK = the register-sink mode (parallel.hpp:181-198): nothing is stored;
 // each thread folds (pos+1)*mix64(key) over its outputs and the CTA adds its
 // partial sum into *sum.
@@ -252,70 +283,70 @@ __global__ void __launch_bounds__(NT)
                        uint32_t *__restrict__ outv,
                        unsigned long long *__restrict__ sum = nullptr) {
   using T = typename KT::T;
-  constexpr int KS = sizeof(T);
+  constexpr uint32_t KS = sizeof(T);
   extern __shared__ __align__(128) char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-  char *base = smem + 16;
   const int tid = threadIdx.x;
 
   const TileWin win = map.window(blockIdx.x);
   const int na_t = win.na, nb_t = win.nb, total = na_t + nb_t;
 
-  // --- smem layout: each window congruent (mod 16) to its global source ---
-  ByteRange rg[4];
-  int nr = 2;
-  rg[0].src = reinterpret_cast<const char *>(a + win.a0);
-  rg[0].bytes = static_cast<uint32_t>(na_t) * KS;
-  rg[0].dst = base + (reinterpret_cast<uintptr_t>(rg[0].src) & 15);
-  rg[1].src = reinterpret_cast<const char *>(b + win.b0);
-  rg[1].bytes = static_cast<uint32_t>(nb_t) * KS;
-  rg[1].dst = align16p(rg[0].dst + rg[0].bytes) +
-              (reinterpret_cast<uintptr_t>(rg[1].src) & 15);
+  // --- smem layout (byte offsets): each window congruent mod 16 to its
+  //     global source, so its 16 B-aligned interior is one bulk copy ---
+  const char *gA = reinterpret_cast<const char *>(a + win.a0);
+  const char *gB = reinterpret_cast<const char *>(b + win.b0);
+  const uint32_t bA = na_t * KS, bB = nb_t * KS;
+  const uint32_t oA = mirror_off(16, gA);
+  const uint32_t oB = mirror_off(oA + bA, gB);
+  const char *gAv = nullptr, *gBv = nullptr;
+  uint32_t oAv = 0, oBv = 0;
   if constexpr (VALS) {
-    nr = 4;
-    rg[2].src = reinterpret_cast<const char *>(av + win.a0);
-    rg[2].bytes = static_cast<uint32_t>(na_t) * 4;
-    rg[2].dst = align16p(rg[1].dst + rg[1].bytes) +
-                (reinterpret_cast<uintptr_t>(rg[2].src) & 15);
-    rg[3].src = reinterpret_cast<const char *>(bv + win.b0);
-    rg[3].bytes = static_cast<uint32_t>(nb_t) * 4;
-    rg[3].dst = align16p(rg[2].dst + rg[2].bytes) +
-                (reinterpret_cast<uintptr_t>(rg[3].src) & 15);
+    gAv = reinterpret_cast<const char *>(av + win.a0);
+    gBv = reinterpret_cast<const char *>(bv + win.b0);
+    oAv = mirror_off(oB + bB, gAv);
+    oBv = mirror_off(oAv + na_t * 4, gBv);
   }
 
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
-    uint32_t tx = 0, lo, hi;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-      if (r < nr)
-        tx += bulk_interior(rg[r], &lo, &hi);
-    mbar_arrive_expect_tx(bar, tx);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      if (r < nr && bulk_interior(rg[r], &lo, &hi))
-        bulk_g2s(rg[r].dst + lo, rg[r].src + lo, hi - lo, bar);
+    uint32_t loA, loB, loAv = 0, loBv = 0;
+    const uint32_t iA = interior_bytes(gA, bA, &loA);
+    const uint32_t iB = interior_bytes(gB, bB, &loB);
+    uint32_t iAv = 0, iBv = 0;
+    if constexpr (VALS) {
+      iAv = interior_bytes(gAv, na_t * 4, &loAv);
+      iBv = interior_bytes(gBv, nb_t * 4, &loBv);
+    }
+    mbar_arrive_expect_tx(bar, iA + iB + iAv + iBv);
+    if (iA)
+      bulk_g2s(smem + oA + loA, gA + loA, iA, bar);
+    if (iB)
+      bulk_g2s(smem + oB + loB, gB + loB, iB, bar);
+    if constexpr (VALS) {
+      if (iAv)
+        bulk_g2s(smem + oAv + loAv, gAv + loAv, iAv, bar);
+      if (iBv)
+        bulk_g2s(smem + oBv + loBv, gBv + loBv, iBv, bar);
     }
   }
+  // unaligned heads/tails: warp 0 takes A, warp 1 takes B (values: 2, 3)
   {
-    uint32_t lo, hi;
-    bulk_interior(rg[0], &lo, &hi);
-    copy_edges<KS, NT>(rg[0], lo, hi);
-    bulk_interior(rg[1], &lo, &hi);
-    copy_edges<KS, NT>(rg[1], lo, hi);
+    const int w = tid >> 5, l = tid & 31;
+    static_assert(NT >= 128, "edge staging uses warps 0..3");
+    if (w == 0)
+      stage_edges<KS>(smem, oA, gA, bA, l);
+    else if (w == 1)
+      stage_edges<KS>(smem, oB, gB, bB, l);
     if constexpr (VALS) {
-      bulk_interior(rg[2], &lo, &hi);
-      copy_edges<4, NT>(rg[2], lo, hi);
-      bulk_interior(rg[3], &lo, &hi);
-      copy_edges<4, NT>(rg[3], lo, hi);
+      if (w == 2)
+        stage_edges<4>(smem, oAv, gAv, na_t * 4, l);
+      else if (w == 3)
+        stage_edges<4>(smem, oBv, gBv, nb_t * 4, l);
     }
   }
   __syncthreads();
   mbar_wait(bar, 0);
-
-  const T *sA = reinterpret_cast<const T *>(rg[0].dst);
-  const T *sB = reinterpret_cast<const T *>(rg[1].dst);
 
   // --- split the window among threads: diagonal search in smem ---
   const int diag = min(tid * VT, total);
@@ -323,37 +354,34 @@ __global__ void __launch_bounds__(NT)
   int hi = diag < na_t ? diag : na_t;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (take_b<KT>(sB[diag - 1 - mid], sA[mid]))
+    if (take_b<KT>(lds<T>(smem, oB + (diag - 1 - mid) * KS),
+                   lds<T>(smem, oA + mid * KS)))
       hi = mid;
     else
       lo = mid + 1;
   }
   int i = lo, j = diag - lo;
 
-  // --- serial stable merge of VT outputs (core.hpp:166-176) ---
+  // --- serial stable merge of VT outputs (core.hpp:166-176), branchless:
+  //     one predicated choice and ONE smem load (the consumed side's next
+  //     element) per output.  Reads may run one element past a window
+  //     (into the next window or the slack) but are never used. ---
   T keys[VT];
   uint32_t vals[VT];
-  T ka = i < na_t ? sA[i] : T{};
-  T kb = j < nb_t ? sB[j] : T{};
+  T ka = lds<T>(smem, oA + min(i, na_t) * KS);
+  T kb = lds<T>(smem, oB + min(j, nb_t) * KS);
 #pragma unroll
   for (int k = 0; k < VT; ++k) {
     const bool tb = (j < nb_t) && ((i >= na_t) || take_b<KT>(kb, ka));
     keys[k] = tb ? kb : ka;
-    if constexpr (VALS) {
-      const uint32_t *sAv = reinterpret_cast<const uint32_t *>(rg[2].dst);
-      const uint32_t *sBv = reinterpret_cast<const uint32_t *>(rg[3].dst);
-      if (diag + k < total)
-        vals[k] = tb ? sBv[j] : sAv[i];
-    }
-    if (tb) {
-      ++j;
-      if (j < nb_t)
-        kb = sB[j];
-    } else {
-      ++i;
-      if (i < na_t)
-        ka = sA[i];
-    }
+    if constexpr (VALS)
+      vals[k] = lds<uint32_t>(smem, tb ? oBv + min(j, nb_t) * 4u
+                                       : oAv + min(i, na_t) * 4u);
+    i += tb ? 0 : 1;
+    j += tb ? 1 : 0;
+    const T nxt = lds<T>(smem, tb ? oB + min(j, nb_t) * KS : oA + min(i, na_t) * KS);
+    kb = tb ? nxt : kb;
+    ka = tb ? ka : nxt;
   }
   if constexpr (SINK) {
     unsigned long long acc = 0;
@@ -379,14 +407,13 @@ __global__ void __launch_bounds__(NT)
   }
   __syncthreads();  // all windows consumed; reuse smem for output staging
 
-  T *stage = reinterpret_cast<T *>(base);
-  uint32_t *stagev = reinterpret_cast<uint32_t *>(
-      align16p(base + stage_elems<NT, VT>() * KS));
+  constexpr uint32_t oS = 16;
+  constexpr uint32_t oSv = (oS + stage_elems<NT, VT>() * KS + 15u) & ~15u;
 #pragma unroll
   for (int k = 0; k < VT; ++k) {
-    stage[stage_idx<VT>(tid * VT + k)] = keys[k];
+    *reinterpret_cast<T *>(smem + oS + stage_idx<VT>(tid * VT + k) * KS) = keys[k];
     if constexpr (VALS)
-      stagev[stage_idx<VT>(tid * VT + k)] = vals[k];
+      *reinterpret_cast<uint32_t *>(smem + oSv + stage_idx<VT>(tid * VT + k) * 4) = vals[k];
   }
 
   T *dst = out + win.o0;
@@ -400,34 +427,68 @@ __global__ void __launch_bounds__(NT)
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      bulk_s2g(dst, stage, static_cast<uint32_t>(total) * KS);
+      bulk_s2g(dst, smem + oS, static_cast<uint32_t>(total) * KS);
       if constexpr (VALS)
-        bulk_s2g(dstv, stagev, static_cast<uint32_t>(total) * 4);
+        bulk_s2g(dstv, smem + oSv, static_cast<uint32_t>(total) * 4);
       bulk_commit();
       bulk_wait_read0();
     }
   } else {
     __syncthreads();
     for (int q = tid; q < total; q += NT) {
-      dst[q] = stage[stage_idx<VT>(q)];
+      dst[q] = lds<T>(smem, oS + stage_idx<VT>(q) * KS);
       if constexpr (VALS)
-        dstv[q] = stagev[stage_idx<VT>(q)];
+        dstv[q] = lds<uint32_t>(smem, oSv + stage_idx<VT>(q) * 4);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
 // K3: stable block sort of NV = NT*VT keys per CTA.
-// Odd-even transposition inside each thread (strict swaps => stable), then
-// log2(NT) Merge Path passes in smem.  Short last block is padded with the
-// maximum key; padding sits at the highest positions so stability keeps it
-// behind every real key.
+// 1) each thread sorts its VT keys in registers: an odd-even transposition
+//    network with strict swaps (stable; needed when values or the element
+//    tag are visible), or a Batcher odd-even merge network of min/max for
+//    bare keys (equal bare keys are indistinguishable, so the bytes are the
+//    same as a stable sort's);
+// 2) log2(NT) Merge Path passes in smem: each thread finds its split on its
+//    pair's cross diagonal and merges VT outputs branch-free.
+// smem index p is padded to p + p/32, which spreads the stride-VT and
+// stride-VT/2 access patterns over all 32 banks.  A short last block is
+// padded with the maximum key; padding sits at the highest positions, so
+// stability keeps it behind every real key.
 // ---------------------------------------------------------------------------
 template <class KT, bool VALS, int NT, int VT>
 __host__ __device__ constexpr uint32_t block_sort_smem_bytes() {
   using T = typename KT::T;
   constexpr uint32_t E = NT * VT + (NT * VT) / 32;
-  return E * sizeof(T) + 16 + (VALS ? E * 4 : 0);
+  return ((E * sizeof(T) + 15) & ~15u) + (VALS ? E * 4 : 0);
+}
+
+template <class KT>
+__device__ __forceinline__ void ce_minmax(typename KT::T &x, typename KT::T &y) {
+  const bool sw = KT::less(y, x);
+  const typename KT::T lo = sw ? y : x;
+  y = sw ? x : y;
+  x = lo;
+}
+
+// Batcher odd-even merge sort network on a register array (n = power of 2).
+template <class KT, int N>
+__device__ __forceinline__ void batcher_sort(typename KT::T (&x)[N]) {
+#pragma unroll
+  for (int p = 1; p < N; p <<= 1) {
+#pragma unroll
+    for (int k = p; k >= 1; k >>= 1) {
+#pragma unroll
+      for (int j = k % p; j + k < N; j += 2 * k) {
+#pragma unroll
+        for (int i = 0; i < k; ++i) {
+          if (i + j + k < N && (i + j) / (2 * p) == (i + j + k) / (2 * p))
+            ce_minmax<KT>(x[i + j], x[i + j + k]);
+        }
+      }
+    }
+  }
 }
 
 template <class KT, bool VALS, int NT, int VT>
@@ -438,19 +499,25 @@ __global__ void __launch_bounds__(NT)
                       uint32_t *__restrict__ outv, uint64_t n) {
   using T = typename KT::T;
   constexpr int NV = NT * VT;
+  constexpr uint32_t KS = sizeof(T);
   constexpr int E = NV + NV / 32;
+  constexpr uint32_t oV = (E * KS + 15) & ~15u;  // values after keys
+  constexpr bool kStable = VALS || KT::kind == kElement;
   extern __shared__ __align__(128) char smem[];
-  T *sk = reinterpret_cast<T *>(smem);
-  uint32_t *sv = reinterpret_cast<uint32_t *>(align16p(smem + E * sizeof(T)));
   const int tid = threadIdx.x;
   const uint64_t base = uint64_t(blockIdx.x) * NV;
   const int cnt = static_cast<int>((n - base) < NV ? (n - base) : NV);
-  auto sidx = [](int p) { return p + (p >> 5); };
+  auto sk = [&](int p) -> T & {
+    return *reinterpret_cast<T *>(smem + (p + (p >> 5)) * KS);
+  };
+  auto sv = [&](int p) -> uint32_t & {
+    return *reinterpret_cast<uint32_t *>(smem + oV + (p + (p >> 5)) * 4);
+  };
 
   for (int q = tid; q < NV; q += NT) {
-    sk[sidx(q)] = q < cnt ? in[base + q] : KT::max_key();
+    sk(q) = q < cnt ? in[base + q] : KT::max_key();
     if constexpr (VALS)
-      sv[sidx(q)] = q < cnt ? inv[base + q] : 0u;
+      sv(q) = q < cnt ? inv[base + q] : 0u;
   }
   __syncthreads();
 
@@ -458,25 +525,28 @@ __global__ void __launch_bounds__(NT)
   uint32_t v[VT];
 #pragma unroll
   for (int k = 0; k < VT; ++k) {
-    x[k] = sk[sidx(tid * VT + k)];
+    x[k] = sk(tid * VT + k);
     if constexpr (VALS)
-      v[k] = sv[sidx(tid * VT + k)];
+      v[k] = sv(tid * VT + k);
   }
+  if constexpr (kStable) {
 #pragma unroll
-  for (int pass = 0; pass < VT; ++pass) {
+    for (int pass = 0; pass < VT; ++pass) {
 #pragma unroll
-    for (int k = pass & 1; k + 1 < VT; k += 2) {
-      if (KT::less(x[k + 1], x[k])) {
-        const T t = x[k];
-        x[k] = x[k + 1];
-        x[k + 1] = t;
+      for (int k = pass & 1; k + 1 < VT; k += 2) {
+        const bool sw = KT::less(x[k + 1], x[k]);
+        const T lo = sw ? x[k + 1] : x[k];
+        x[k + 1] = sw ? x[k] : x[k + 1];
+        x[k] = lo;
         if constexpr (VALS) {
-          const uint32_t tv = v[k];
-          v[k] = v[k + 1];
-          v[k + 1] = tv;
+          const uint32_t lv = sw ? v[k + 1] : v[k];
+          v[k + 1] = sw ? v[k] : v[k + 1];
+          v[k] = lv;
         }
       }
     }
+  } else {
+    batcher_sort<KT, VT>(x);
   }
 
 #pragma unroll 1
@@ -484,56 +554,52 @@ __global__ void __launch_bounds__(NT)
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < VT; ++k) {
-      sk[sidx(tid * VT + k)] = x[k];
+      sk(tid * VT + k) = x[k];
       if constexpr (VALS)
-        sv[sidx(tid * VT + k)] = v[k];
+        sv(tid * VT + k) = v[k];
     }
     __syncthreads();
-    const int gs = ((tid * VT) / (2 * width)) * (2 * width);
+    const int gs = (tid * VT) & ~(2 * width - 1);
     const int diag = tid * VT - gs;
     const int A0 = gs, B0 = gs + width;
     int lo = diag > width ? diag - width : 0;
     int hi = diag < width ? diag : width;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (take_b<KT>(sk[sidx(B0 + diag - 1 - mid)], sk[sidx(A0 + mid)]))
+      if (take_b<KT>(sk(B0 + diag - 1 - mid), sk(A0 + mid)))
         hi = mid;
       else
         lo = mid + 1;
     }
     int i = lo, j = diag - lo;
-    T ka = sk[sidx(A0 + (i < width ? i : width - 1))];
-    T kb = sk[sidx(B0 + (j < width ? j : width - 1))];
+    T ka = sk(A0 + min(i, width - 1));
+    T kb = sk(B0 + min(j, width - 1));
 #pragma unroll
     for (int k = 0; k < VT; ++k) {
       const bool tb = (j < width) && ((i >= width) || take_b<KT>(kb, ka));
       x[k] = tb ? kb : ka;
       if constexpr (VALS)
-        v[k] = tb ? sv[sidx(B0 + j)] : sv[sidx(A0 + i)];
-      if (tb) {
-        ++j;
-        if (j < width)
-          kb = sk[sidx(B0 + j)];
-      } else {
-        ++i;
-        if (i < width)
-          ka = sk[sidx(A0 + i)];
-      }
+        v[k] = sv(tb ? B0 + j : A0 + i);
+      i += tb ? 0 : 1;
+      j += tb ? 1 : 0;
+      const T nxt = sk(tb ? B0 + min(j, width - 1) : A0 + min(i, width - 1));
+      kb = tb ? nxt : kb;
+      ka = tb ? ka : nxt;
     }
   }
 
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < VT; ++k) {
-    sk[sidx(tid * VT + k)] = x[k];
+    sk(tid * VT + k) = x[k];
     if constexpr (VALS)
-      sv[sidx(tid * VT + k)] = v[k];
+      sv(tid * VT + k) = v[k];
   }
   __syncthreads();
   for (int q = tid; q < cnt; q += NT) {
-    out[base + q] = sk[sidx(q)];
+    out[base + q] = sk(q);
     if constexpr (VALS)
-      outv[base + q] = sv[sidx(q)];
+      outv[base + q] = sv(q);
   }
 }
 
