@@ -117,9 +117,34 @@ uint64_t mp_sort_scratch_bytes(int key_type, int with_vals, uint64_t n);
 int mp_sort(int key_type, void *keys, uint32_t *vals, uint64_t n,
             void *scratch, uint64_t scratch_bytes, void *stream);
 
+/* ---- segmented-merge schedule (parallel.hpp:90-145, :258-292) --------- */
+/* Windows of L = cache_elems/3 outputs; ceil((na+nb)/L) of them.
+ * start_a[k] (device) = a_off where window k starts (diagonal k*L).
+ * plan_comparisons / merge_comparisons (device uint64, may be NULL)
+ * accumulate the reference's counters: plan_segments' end-of-window
+ * searches and the p_eff window-local worker searches of
+ * segmented_parallel_merge.  p == 0 or cache_elems < 3 -> MP_ERR_INVALID. */
+uint64_t mp_segment_iterations(uint64_t na, uint64_t nb, uint64_t cache_elems);
+int mp_segment_plan(int key_type, const void *a, uint64_t na, const void *b,
+                    uint64_t nb, uint64_t p, uint64_t cache_elems,
+                    uint64_t *start_a, uint64_t *plan_comparisons,
+                    uint64_t *merge_comparisons, void *stream);
+
 /* ---- host-buffer entry points (synchronous) --------------------------- */
+/* Counters (`comparisons`, `*_comparisons`) are host uint64 here, may be
+ * NULL, and accumulate (+=) like the reference's stats pointers. */
 int mp_partition_host(int key_type, const void *a, uint64_t na, const void *b,
-                      uint64_t nb, uint64_t p, uint64_t *a_offs, int device);
+                      uint64_t nb, uint64_t p, uint64_t *a_offs,
+                      uint64_t *comparisons, int device);
+int mp_diagonal_search_host(int key_type, const void *a, uint64_t na,
+                            const void *b, uint64_t nb, const uint64_t *diags,
+                            uint64_t count, uint64_t *a_offs,
+                            uint64_t *comparisons, int device);
+int mp_segment_plan_host(int key_type, const void *a, uint64_t na,
+                         const void *b, uint64_t nb, uint64_t p,
+                         uint64_t cache_elems, uint64_t *start_a,
+                         uint64_t *start_b, uint64_t *plan_comparisons,
+                         uint64_t *merge_comparisons, int device);
 int mp_merge_host(int key_type, const void *a, const uint32_t *a_vals,
                   uint64_t na, const void *b, const uint32_t *b_vals,
                   uint64_t nb, void *out, uint32_t *out_vals, int device);

@@ -35,7 +35,11 @@ SIGNATURES = [
     ("mp_merge_checksum", _i, [_i, _p, _u64, _p, _u64, _p, _p]),
     ("mp_sort_scratch_bytes", _u64, [_i, _i, _u64]),
     ("mp_sort", _i, [_i, _p, _p, _u64, _p, _u64, _p]),
-    ("mp_partition_host", _i, [_i, _p, _u64, _p, _u64, _u64, _p, _i]),
+    ("mp_segment_iterations", _u64, [_u64, _u64, _u64]),
+    ("mp_segment_plan", _i, [_i, _p, _u64, _p, _u64, _u64, _u64, _p, _p, _p, _p]),
+    ("mp_partition_host", _i, [_i, _p, _u64, _p, _u64, _u64, _p, _p, _i]),
+    ("mp_diagonal_search_host", _i, [_i, _p, _u64, _p, _u64, _p, _u64, _p, _p, _i]),
+    ("mp_segment_plan_host", _i, [_i, _p, _u64, _p, _u64, _u64, _u64, _p, _p, _p, _p, _i]),
     ("mp_merge_host", _i, [_i, _p, _p, _u64, _p, _p, _u64, _p, _p, _i]),
     ("mp_sort_host", _i, [_i, _p, _p, _u64, _p, _p, _i]),
     ("mp_merge_checksum_host", _i, [_i, _p, _u64, _p, _u64, _p, _i]),

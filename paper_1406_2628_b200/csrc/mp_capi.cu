@@ -431,6 +431,46 @@ template <class KT> struct SortOp {
   }
 };
 
+// Segmented-merge schedule on the device: window starts (K1 at diagonals
+// k*L) and the reference's exact comparison counters.
+template <class KT> struct SegmentOp {
+  static int run(const void *a, uint64_t na, const void *b, uint64_t nb,
+                 uint64_t p, uint64_t L, uint64_t *start_a, uint64_t *plan_cmp,
+                 uint64_t *merge_cmp, uint64_t *scratch_diags,
+                 cudaStream_t s) {
+    using T = typename KT::T;
+    const uint64_t n = na + nb;
+    const uint64_t iters = cdiv(n, L);
+    if (iters == 0)
+      return MP_OK;
+    // window starts = diagonal search at k*L (k = 0..iters-1)
+    if (int rc = launch_partition<KT>(a, na, b, nb, L, 0, iters, start_a, s))
+      return rc;
+    (void)scratch_diags;
+    const uint64_t p_eff = p < L ? p : L;
+    if (plan_cmp || merge_cmp) {
+      ScratchGuard g;
+      unsigned long long *pc = reinterpret_cast<unsigned long long *>(plan_cmp);
+      unsigned long long *mc = reinterpret_cast<unsigned long long *>(merge_cmp);
+      if (!pc || !mc) {
+        if (int rc = alloc_scratch(g, 16, s))
+          return rc;
+        if (!pc)
+          pc = static_cast<unsigned long long *>(g.p);
+        if (!mc)
+          mc = static_cast<unsigned long long *>(g.p) + 1;
+      }
+      const uint64_t threads = iters * (p_eff + 1);
+      segment_stats_kernel<KT>
+          <<<static_cast<unsigned>(cdiv(threads, 128)), 128, 0, s>>>(
+              static_cast<const T *>(a), na, static_cast<const T *>(b), nb, L,
+              p_eff, iters, start_a, pc, mc);
+      MP_LAUNCHED("segment_stats_kernel");
+    }
+    return MP_OK;
+  }
+};
+
 template <class KT> struct ScratchOp {
   static int run(bool vals, uint64_t n, uint64_t *out) {
     *out = n <= 1 ? 0 : sort_layout<KT>(vals, n).total;
@@ -753,33 +793,167 @@ int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,
 }
 
 // ---- host-buffer entry points ----------------------------------------------
+}  // extern "C"
+
+namespace {
+// Stage host A and B (+ `extra` scratch bytes) into one device buffer.
+struct HostInputs {
+  ScratchGuard g;
+  char *a = nullptr, *b = nullptr, *extra = nullptr;
+  int stage(const void *ha, uint64_t na, const void *hb, uint64_t nb,
+            uint64_t ks, uint64_t extra_bytes, cudaStream_t s) {
+    const uint64_t ab = (na * ks + 255) & ~uint64_t(255);
+    const uint64_t bb = (nb * ks + 255) & ~uint64_t(255);
+    if (int rc = alloc_scratch(g, ab + bb + extra_bytes + 16, s))
+      return rc;
+    a = static_cast<char *>(g.p);
+    b = a + ab;
+    extra = b + bb;
+    if (na)
+      MP_CUDA(cudaMemcpyAsync(a, ha, na * ks, cudaMemcpyHostToDevice, s));
+    if (nb)
+      MP_CUDA(cudaMemcpyAsync(b, hb, nb * ks, cudaMemcpyHostToDevice, s));
+    return MP_OK;
+  }
+};
+}  // namespace
+
+extern "C" {
+
 int mp_partition_host(int kt, const void *a, uint64_t na, const void *b,
-                      uint64_t nb, uint64_t p, uint64_t *a_offs, int device) {
+                      uint64_t nb, uint64_t p, uint64_t *a_offs,
+                      uint64_t *comparisons, int device) {
   g_err.clear();
   const uint64_t ks = key_size(kt);
   if (!ks)
     return fail(MP_ERR_UNSUPPORTED, "unknown key type %d", kt);
   if (p == 0)
     return fail(MP_ERR_INVALID, "partition: p must be positive");
+  if (!a_offs)
+    return fail(MP_ERR_INVALID, "partition: a_offs is NULL");
   DeviceScope ds(device);
   if (ds.err != cudaSuccess)
     return cuda_fail(ds.err, "cudaSetDevice");
   cudaStream_t s = host_stream(device);
-  ScratchGuard g;
-  const uint64_t ab = (na * ks + 255) & ~uint64_t(255);
-  const uint64_t bb = (nb * ks + 255) & ~uint64_t(255);
-  if (int rc = alloc_scratch(g, ab + bb + (p + 1) * 8, s))
+  HostInputs in;
+  if (int rc = in.stage(a, na, b, nb, ks, (p + 2) * 8, s))
     return rc;
-  char *d = static_cast<char *>(g.p);
-  if (na)
-    MP_CUDA(cudaMemcpyAsync(d, a, na * ks, cudaMemcpyHostToDevice, s));
-  if (nb)
-    MP_CUDA(cudaMemcpyAsync(d + ab, b, nb * ks, cudaMemcpyHostToDevice, s));
-  uint64_t *offs = reinterpret_cast<uint64_t *>(d + ab + bb);
-  if (int rc = mp_partition(kt, d, na, d + ab, nb, p, offs, nullptr, s))
+  uint64_t *offs = reinterpret_cast<uint64_t *>(in.extra);
+  uint64_t *cnt = offs + p + 1;
+  MP_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
+  if (int rc = mp_partition(kt, in.a, na, in.b, nb, p, offs, cnt, s))
     return rc;
   MP_CUDA(cudaMemcpyAsync(a_offs, offs, (p + 1) * 8, cudaMemcpyDeviceToHost, s));
+  uint64_t c = 0;
+  MP_CUDA(cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaStreamSynchronize(s));
+  if (comparisons)
+    *comparisons += c;
+  return MP_OK;
+}
+
+int mp_diagonal_search_host(int kt, const void *a, uint64_t na, const void *b,
+                            uint64_t nb, const uint64_t *diags, uint64_t count,
+                            uint64_t *a_offs, uint64_t *comparisons,
+                            int device) {
+  g_err.clear();
+  const uint64_t ks = key_size(kt);
+  if (!ks)
+    return fail(MP_ERR_UNSUPPORTED, "unknown key type %d", kt);
+  if (count == 0)
+    return MP_OK;
+  if (!diags || !a_offs)
+    return fail(MP_ERR_INVALID, "diagonal_search: NULL array");
+  DeviceScope ds(device);
+  if (ds.err != cudaSuccess)
+    return cuda_fail(ds.err, "cudaSetDevice");
+  cudaStream_t s = host_stream(device);
+  HostInputs in;
+  if (int rc = in.stage(a, na, b, nb, ks, (2 * count + 1) * 8, s))
+    return rc;
+  uint64_t *dd = reinterpret_cast<uint64_t *>(in.extra);
+  uint64_t *offs = dd + count;
+  uint64_t *cnt = offs + count;
+  MP_CUDA(cudaMemcpyAsync(dd, diags, count * 8, cudaMemcpyHostToDevice, s));
+  MP_CUDA(cudaMemsetAsync(cnt, 0, 8, s));
+  if (int rc = mp_diagonal_search(kt, in.a, na, in.b, nb, dd, count, offs, cnt, s))
+    return rc;
+  MP_CUDA(cudaMemcpyAsync(a_offs, offs, count * 8, cudaMemcpyDeviceToHost, s));
+  uint64_t c = 0;
+  MP_CUDA(cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  if (comparisons)
+    *comparisons += c;
+  return MP_OK;
+}
+
+uint64_t mp_segment_iterations(uint64_t na, uint64_t nb, uint64_t cache_elems) {
+  if (cache_elems < 3)
+    return 0;
+  const uint64_t L = cache_elems / 3;
+  return (na + nb + L - 1) / L;
+}
+
+int mp_segment_plan(int kt, const void *a, uint64_t na, const void *b,
+                    uint64_t nb, uint64_t p, uint64_t cache_elems,
+                    uint64_t *start_a, uint64_t *plan_comparisons,
+                    uint64_t *merge_comparisons, void *stream) {
+  g_err.clear();
+  if (p == 0)
+    return fail(MP_ERR_INVALID, "merge: worker count must be positive");
+  if (cache_elems < 3)
+    return fail(MP_ERR_INVALID, "merge: cache capacity must be at least 3");
+  if ((na + nb) && !start_a)
+    return fail(MP_ERR_INVALID, "segment_plan: NULL start array");
+  return dispatch<SegmentOp>(kt, a, na, b, nb, p, cache_elems / 3, start_a,
+                             plan_comparisons, merge_comparisons,
+                             static_cast<uint64_t *>(nullptr),
+                             static_cast<cudaStream_t>(stream));
+}
+
+int mp_segment_plan_host(int kt, const void *a, uint64_t na, const void *b,
+                         uint64_t nb, uint64_t p, uint64_t cache_elems,
+                         uint64_t *start_a, uint64_t *start_b,
+                         uint64_t *plan_comparisons,
+                         uint64_t *merge_comparisons, int device) {
+  g_err.clear();
+  const uint64_t ks = key_size(kt);
+  if (!ks)
+    return fail(MP_ERR_UNSUPPORTED, "unknown key type %d", kt);
+  if (p == 0)
+    return fail(MP_ERR_INVALID, "merge: worker count must be positive");
+  if (cache_elems < 3)
+    return fail(MP_ERR_INVALID, "merge: cache capacity must be at least 3");
+  const uint64_t iters = mp_segment_iterations(na, nb, cache_elems);
+  if (iters == 0)
+    return MP_OK;
+  if (!start_a)
+    return fail(MP_ERR_INVALID, "segment_plan: NULL start array");
+  DeviceScope ds(device);
+  if (ds.err != cudaSuccess)
+    return cuda_fail(ds.err, "cudaSetDevice");
+  cudaStream_t s = host_stream(device);
+  HostInputs in;
+  if (int rc = in.stage(a, na, b, nb, ks, (iters + 2) * 8, s))
+    return rc;
+  uint64_t *st = reinterpret_cast<uint64_t *>(in.extra);
+  uint64_t *cnt = st + iters;
+  MP_CUDA(cudaMemsetAsync(cnt, 0, 16, s));
+  if (int rc = mp_segment_plan(kt, in.a, na, in.b, nb, p, cache_elems, st, cnt,
+                               cnt + 1, s))
+    return rc;
+  MP_CUDA(cudaMemcpyAsync(start_a, st, iters * 8, cudaMemcpyDeviceToHost, s));
+  uint64_t c[2] = {0, 0};
+  MP_CUDA(cudaMemcpyAsync(c, cnt, 16, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  const uint64_t L = cache_elems / 3;
+  if (start_b)
+    for (uint64_t k = 0; k < iters; ++k)
+      start_b[k] = k * L - start_a[k];
+  if (plan_comparisons)
+    *plan_comparisons += c[0];
+  if (merge_comparisons)
+    *merge_comparisons += c[1];
   return MP_OK;
 }
 

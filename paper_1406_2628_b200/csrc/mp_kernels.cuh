@@ -273,8 +273,25 @@ __device__ __forceinline__ T lds(const char *smem, uint32_t off) {
 // SINK = the register-sink mode (parallel.hpp:181-198): nothing is stored;
 // each thread folds (pos+1)*mix64(key) over its outputs and the CTA adds its
 // partial sum into *sum.
+// Residency target: a full SM (2048 threads, <= 32 registers) for bare
+// keys up to 8 B; 3/4 of it when values or 16-byte elements ride along.
+template <class KT, bool VALS, int NT, bool SINK = false>
+constexpr int merge_min_blocks() {
+  return (VALS || SINK)                             ? 1280 / NT
+         : sizeof(typename KT::T) == 4 && KT::kind != kF32 ? 2048 / NT
+         : sizeof(typename KT::T) <= 8               ? 1536 / NT
+                                                     : 1280 / NT;
+}
+template <class KT, bool VALS, int NT>
+constexpr int block_sort_min_blocks() {
+  return sizeof(typename KT::T) > 8   ? 512 / NT
+         : VALS                        ? 1024 / NT
+         : sizeof(typename KT::T) == 4 ? 2048 / NT
+                                       : 1024 / NT;
+}
+
 template <class KT, bool VALS, int NT, int VT, class Map, bool SINK = false>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
     merge_tiles_kernel(Map map, const typename KT::T *__restrict__ a,
                        const uint32_t *__restrict__ av,
                        const typename KT::T *__restrict__ b,
@@ -492,7 +509,7 @@ __device__ __forceinline__ void batcher_sort(typename KT::T (&x)[N]) {
 }
 
 template <class KT, bool VALS, int NT, int VT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, (block_sort_min_blocks<KT, VALS, NT>()))
     block_sort_kernel(const typename KT::T *__restrict__ in,
                       const uint32_t *__restrict__ inv,
                       typename KT::T *__restrict__ out,
@@ -600,6 +617,56 @@ __global__ void __launch_bounds__(NT)
     out[base + q] = sk(q);
     if constexpr (VALS)
       outv[base + q] = sv(q);
+  }
+}
+
+}  // namespace mpb
+
+namespace mpb {
+
+// ---------------------------------------------------------------------------
+// Statistics of the Segmented Parallel Merge schedule (parallel.hpp:90-145,
+// :262-292), computed on the device so drop-in callers get the reference's
+// exact counters.  Window k starts on global diagonal k*L (the reference
+// proves this equivalence, test_parallel.cpp:120-137), with its start split
+// in starts_a[k].  Thread (k, r): r < p_eff replays worker r's window-local
+// search; r == p_eff replays plan_segments' end-of-window search.
+// ---------------------------------------------------------------------------
+template <class KT>
+__global__ void segment_stats_kernel(const typename KT::T *__restrict__ a,
+                                     uint64_t na,
+                                     const typename KT::T *__restrict__ b,
+                                     uint64_t nb, uint64_t L, uint64_t p_eff,
+                                     uint64_t iters,
+                                     const uint64_t *__restrict__ starts_a,
+                                     unsigned long long *__restrict__ plan_cmp,
+                                     unsigned long long *__restrict__ merge_cmp) {
+  const uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const uint64_t k = idx / (p_eff + 1), r = idx % (p_eff + 1);
+  if (k >= iters)
+    return;
+  const uint64_t n = na + nb;
+  const uint64_t d0 = k * L;
+  const uint64_t ca = starts_a[k], cb = d0 - ca;
+  const uint64_t rest = n - d0;
+  const uint64_t Lw = L < rest ? L : rest;
+  const uint64_t sna = Lw < na - ca ? Lw : na - ca;
+  const uint64_t snb = Lw < nb - cb ? Lw : nb - cb;
+  uint32_t c = 0;
+  if (r == p_eff) {
+    if (k + 1 == iters)
+      return;
+    diag_search_global<KT>(a + ca, sna, b + cb, snb, Lw, &c);
+    if (c)
+      atomicAdd(plan_cmp, static_cast<unsigned long long>(c));
+  } else {
+    const uint64_t pw = p_eff < Lw ? p_eff : Lw;
+    if (r >= pw)
+      return;
+    const uint64_t dl = (r * Lw) / pw;
+    diag_search_global<KT>(a + ca, sna, b + cb, snb, dl, &c);
+    if (c)
+      atomicAdd(merge_cmp, static_cast<unsigned long long>(c));
   }
 }
 

@@ -300,29 +300,54 @@ def parallel_merge(a, b, p: int = 1, comp=None, stats: MergeStats | None = None,
     return (out, out_vals) if out_vals is not None else out
 
 
+def _segment_plan(A: _Arr, B: _Arr, p: int, cache_elems: int):
+    """Window starts + the reference's two comparison counters, computed on
+    the device by mp_segment_plan (window k starts on diagonal k*L,
+    test_parallel.cpp:120-137)."""
+    iters = int(N.lib.mp_segment_iterations(A.n, B.n, cache_elems))
+    L = cache_elems // 3
+    if iters == 0:
+        return [], 0, 0
+    if A.device:
+        st = torch.empty(iters, dtype=torch.int64, device=A.obj.device)
+        cnt = torch.zeros(2, dtype=torch.int64, device=A.obj.device)
+        N.check(N.lib.mp_segment_plan(A.kt, A.ptr, A.n, B.ptr, B.n, p, cache_elems,
+                                      st.data_ptr(), cnt.data_ptr(), cnt.data_ptr() + 8,
+                                      _stream_ptr(A)))
+        sa = st.cpu().tolist()
+        plan_cmp, merge_cmp = cnt.cpu().tolist()
+    else:
+        st = np.zeros(iters, dtype=np.uint64)
+        pc, mc = C.c_uint64(0), C.c_uint64(0)
+        N.check(N.lib.mp_segment_plan_host(A.kt, A.ptr, A.n, B.ptr, B.n, p, cache_elems,
+                                           st.ctypes.data, None, C.byref(pc), C.byref(mc), 0))
+        sa = st.tolist()
+        plan_cmp, merge_cmp = pc.value, mc.value
+    starts = [PartitionPoint(int(x), k * L - int(x)) for k, x in enumerate(sa)]
+    return starts, plan_cmp, merge_cmp
+
+
 def plan_segments(a, b, p: int, cache_elems: int, comparisons: list | None = None,
                   key_type=None) -> SegmentPlan:
-    """parallel.hpp:258-292.  Window k starts at diagonal_search(k*L)
-    (test_parallel.cpp:120-137); all starts come from one device search."""
+    """parallel.hpp:258-292: window geometry and every window's starting
+    point; `comparisons` accumulates the reference's search count."""
     _check_p(p)
     L = _window_of(cache_elems)
     A, B = _pair(a, b, key_type)
-    n = A.n + B.n
-    iters = (n + L - 1) // L
-    plan = SegmentPlan(cache_elems, L, min(p, L), iters, [])
-    if iters:
-        plan.starting_points = [PartitionPoint(0, 0)] + _search(
-            A, B, [k * L for k in range(1, iters)], comparisons)
-    return plan
+    starts, plan_cmp, _ = _segment_plan(A, B, p, cache_elems)
+    if comparisons is not None:
+        comparisons[0] += plan_cmp
+    return SegmentPlan(cache_elems, L, min(p, L), len(starts), starts)
 
 
 def _segmented_stats(A, B, p, cache_elems, stats):
     if stats is None:
         return
-    plan = plan_segments(A.obj, B.obj, p, cache_elems, key_type=A.kt)
+    starts, _, merge_cmp = _segment_plan(A, B, p, cache_elems)
     stats.merge_steps += A.n + B.n
-    ends = plan.starting_points[1:] + [PartitionPoint(A.n, B.n)]
-    for s, e in zip(plan.starting_points, ends):
+    stats.partition_comparisons += merge_cmp
+    ends = starts[1:] + [PartitionPoint(A.n, B.n)]
+    for s, e in zip(starts, ends):
         stats.windows.append(WindowStats(e.a_off - s.a_off, e.b_off - s.b_off))
 
 

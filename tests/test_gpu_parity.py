@@ -116,9 +116,12 @@ def test_fixture_partitions_and_stats(cuda, fixtures):
             mp.segmented_parallel_merge(a, b, p, C, stats=st, key_type=kt)
             wins = [[w.a_consumed, w.b_consumed] for w in st.windows]
             assert wins == fixtures[k + f"/seg{p}_{C}"].tolist(), (k, p, C)
-            plan = mp.plan_segments(a, b, p, C, key_type=kt)
+            assert [st.partition_comparisons, st.merge_steps] == \
+                fixtures[k + f"/segstats{p}_{C}"].tolist(), (k, p, C)
+            cnt = [0]
+            plan = mp.plan_segments(a, b, p, C, comparisons=cnt, key_type=kt)
             ref = fixtures[k + f"/plan{p}_{C}"].tolist()
-            assert [plan.window_len, plan.p_eff, plan.iterations] == ref[:3]
+            assert [plan.window_len, plan.p_eff, plan.iterations, cnt[0]] == ref, (k, p, C)
             assert [[s.a_off, s.b_off] for s in plan.starting_points] == \
                 fixtures[k + f"/planstarts{p}_{C}"].tolist(), (k, p, C)
 
