@@ -1,0 +1,492 @@
+"""Multi-GPU Merge Path: one process per GPU over torch.distributed.
+
+Theorem 14 / Corollary 6 of the paper applied at
+GPU granularity: the merged output S is cut into P equal slices on the
+cross diagonals d_r = floor(r*N/P); rank r finds its split (a_r, b_r) on
+d_r, pulls A[a_r, a_{r+1}) and B[b_r, b_{r+1}) from whichever ranks own
+them, and merges them locally with the single-GPU kernels.  Writes are
+disjoint, so there is exactly ONE exchange per merge and no other
+communication.
+
+The three steps map onto the B200 box as:
+
+  1. split search   -- all P-1 interior diagonals are searched jointly with a
+                       K-ary search: per step every rank knows every probe
+                       position (the state is replicated), fills the probe
+                       keys it owns from its local shard (a device gather)
+                       and one all_reduce(SUM) delivers them all.  A 2^31
+                       diagonal needs ceil(31 / log2 K) steps (K = 64: 6).
+  2. exchange       -- the split points give every (owner, receiver) slice;
+                       one all_to_all_single per array (keys, then values)
+                       moves them: NCCL grouped send/recv over NVLink 5 /
+                       NVSwitch on the GPU box, gloo in the CPU tests.
+  3. local merge    -- mp_merge on the received contiguous A and B ranges.
+
+Sorting (config 4 at P GPUs): each rank sorts its shard with mp_sort, then
+ceil(log2 P) rounds merge pairs of sorted rank-blocks with the same
+sharded merge (left block = A, so the sort stays stable w.r.t. input order;
+an unpaired last block is carried, as in sort.hpp:98-100).
+
+The host logic here is backend-agnostic; the GPU-side work is the
+library's kernels.  `local_merge` / `local_sort` hooks exist so the CPU
+test-suite can run the distributed host logic over gloo with a checker in
+place of the device kernels.
+"""
+from __future__ import annotations
+
+import bisect
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+K_ARY = 64  # probes per search step = K_ARY - 1
+
+
+# --------------------------------------------------------------------------
+# keys: order-preserving int64 image (so torch int64 compares implement the
+# library's comparator: unsigned, signed, IEEE totalOrder, element key)
+# --------------------------------------------------------------------------
+def key_type_of(t: torch.Tensor, key_type=None) -> int:
+    if key_type is not None:
+        return key_type
+    m = {torch.uint32: N.KEY_U32, torch.int32: N.KEY_I32, torch.float32: N.KEY_F32,
+         torch.uint64: N.KEY_U64, torch.int64: N.KEY_I64}
+    if t.dtype not in m:
+        raise TypeError(f"unsupported key dtype {t.dtype}")
+    return m[t.dtype]
+
+
+def _flat_keys(t: torch.Tensor, kt: int) -> torch.Tensor:
+    """Raw key words as a signed integer tensor of one element per key."""
+    if kt in (N.KEY_U32, N.KEY_I32, N.KEY_F32):
+        return t.view(torch.int32)
+    if kt in (N.KEY_U64, N.KEY_I64):
+        return t.view(torch.int64)
+    return t.view(torch.int64).view(-1, 2)[:, 0]  # element: int64 key first
+
+
+def order_image(raw: torch.Tensor, kt: int) -> torch.Tensor:
+    """int64 image whose signed order equals the key order of `kt`."""
+    x = raw.to(torch.int64)
+    if kt == N.KEY_U32:
+        return x & 0xFFFFFFFF
+    if kt == N.KEY_I32:
+        return x
+    if kt == N.KEY_F32:
+        u = x & 0xFFFFFFFF
+        return torch.where((u & 0x80000000) != 0, u ^ 0xFFFFFFFF, u | 0x80000000)
+    if kt == N.KEY_U64:
+        return x ^ torch.iinfo(torch.int64).min
+    return x  # I64, ELEMENT key
+
+
+def n_keys(t: torch.Tensor, kt: int) -> int:
+    return t.numel() * t.element_size() // N.KEY_SIZES[kt]
+
+
+# --------------------------------------------------------------------------
+# jobs: a merge of two sequences, each spread over an ordered list of ranks
+# --------------------------------------------------------------------------
+@dataclass
+class Piece:
+    rank: int
+    start: int   # global index of this piece's first element in its sequence
+    length: int
+
+
+@dataclass
+class Job:
+    a: list          # [Piece] in sequence order (ascending rank)
+    b: list          # [Piece]
+    owners: list     # output ranks in order; slice k = [floor(k*N/m), floor((k+1)*N/m))
+
+    @property
+    def na(self) -> int:
+        return sum(p.length for p in self.a)
+
+    @property
+    def nb(self) -> int:
+        return sum(p.length for p in self.b)
+
+    def diagonal(self, k: int) -> int:
+        n = self.na + self.nb
+        return k * n // len(self.owners)
+
+
+def _pieces(ranks, lengths):
+    out, s = [], 0
+    for r in ranks:
+        out.append(Piece(r, s, int(lengths[r])))
+        s += int(lengths[r])
+    return out
+
+
+def _owner(pieces, idx):
+    starts = [p.start for p in pieces]
+    k = bisect.bisect_right(starts, idx) - 1
+    while pieces[k].length == 0 or idx >= pieces[k].start + pieces[k].length:
+        k += 1
+    return pieces[k], idx - pieces[k].start
+
+
+class _Comm:
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        backend = dist.get_backend(group)
+        self.dev = (torch.device("cuda", torch.cuda.current_device())
+                    if backend == "nccl" else torch.device("cpu"))
+
+    def all_gather_int(self, values):
+        t = torch.tensor(values, dtype=torch.int64, device=self.dev)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return [o.cpu().tolist() for o in out]
+
+    def all_reduce_sum(self, t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def all_to_all(self, send: torch.Tensor, send_counts, recv_counts):
+        # move raw words: signed integer views of the same width are supported
+        # by every backend (gloo has no uint32/uint64 reductions or copies)
+        wire = {1: torch.int8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[
+            send.element_size()]
+        recv = torch.empty(sum(recv_counts), dtype=wire, device=send.device)
+        dist.all_to_all_single(recv, send.view(wire), recv_counts, send_counts,
+                               group=self.group)
+        return recv.view(send.dtype)
+
+
+# --------------------------------------------------------------------------
+# step 1: joint K-ary split search over all interior diagonals of all jobs
+# --------------------------------------------------------------------------
+def distributed_splits(comm: _Comm, jobs, a_local, b_local, kt, k_ary=K_ARY):
+    """For each job, the a_off of the merge path on every owner boundary
+    diagonal (k = 0..m).  Same predicate as the device kernels: move right
+    iff B[d-1-m] < A[m] (ties to A, core.hpp:107-114)."""
+    a_img_src = _flat_keys(a_local, kt) if a_local is not None else None
+    b_img_src = _flat_keys(b_local, kt) if b_local is not None else None
+    # search state: (job, k, d, lo, hi)
+    searches = []
+    result = []
+    for j, job in enumerate(jobs):
+        m = len(job.owners)
+        res = [0] * (m + 1)
+        res[m] = job.na
+        for k in range(1, m):
+            d = job.diagonal(k)
+            lo, hi = max(0, d - job.nb), min(d, job.na)
+            searches.append([j, k, d, lo, hi])
+        result.append(res)
+    while True:
+        active = [s for s in searches if s[3] < s[4]]
+        if not active:
+            break
+        # probe table: for every active search, its probe positions
+        table = []  # (search, m)
+        for s in active:
+            lo, hi = s[3], s[4]
+            span = hi - lo
+            if span <= k_ary - 1:
+                ms = list(range(lo, hi))
+            else:
+                ms = sorted(set(lo + (i * span) // k_ary for i in range(1, k_ary)))
+            for m_ in ms:
+                table.append((s, m_))
+        # fill the probe keys this rank owns: A[m] and B[d-1-m]
+        a_idx, a_pos, b_idx, b_pos = [], [], [], []
+        for t, (s, m_) in enumerate(table):
+            job = jobs[s[0]]
+            pa, off_a = _owner(job.a, m_)
+            if pa.rank == comm.rank:
+                a_idx.append(off_a)
+                a_pos.append(t)
+            pb, off_b = _owner(job.b, s[2] - 1 - m_)
+            if pb.rank == comm.rank:
+                b_idx.append(off_b)
+                b_pos.append(t)
+        vals = torch.zeros(2 * len(table), dtype=torch.int64, device=comm.dev)
+        if a_idx:
+            src = order_image(a_img_src[torch.tensor(a_idx, device=a_img_src.device)], kt)
+            vals[torch.tensor(a_pos, device=comm.dev) * 2] = src.to(comm.dev)
+        if b_idx:
+            src = order_image(b_img_src[torch.tensor(b_idx, device=b_img_src.device)], kt)
+            vals[torch.tensor(b_pos, device=comm.dev) * 2 + 1] = src.to(comm.dev)
+        comm.all_reduce_sum(vals)
+        v = vals.view(-1, 2).cpu()
+        take_b = (v[:, 1] < v[:, 0]).tolist()
+        # narrow every active search: first probe whose predicate is true
+        t = 0
+        for s in active:
+            lo, hi = s[3], s[4]
+            new_lo, new_hi = None, hi
+            prev = lo - 1
+            while t < len(table) and table[t][0] is s:
+                m_ = table[t][1]
+                if new_lo is None and take_b[t]:
+                    new_lo, new_hi = prev + 1, m_
+                prev = m_
+                t += 1
+            if new_lo is None:
+                new_lo = prev + 1
+            s[3], s[4] = new_lo, new_hi
+    for s in searches:
+        result[s[0]][s[1]] = s[3]
+    return result
+
+
+# --------------------------------------------------------------------------
+# step 2: the exchange plan
+# --------------------------------------------------------------------------
+def _send_recv_counts(comm: _Comm, jobs, splits, which):
+    """Counts of `which` ('a'/'b') elements each rank sends to / receives
+    from every other rank, plus this rank's local offsets to send."""
+    P = comm.world
+    send = [0] * P
+    recv = [0] * P
+    send_ranges = [None] * P  # local [lo, hi) sent to each receiver
+    for job, spl in zip(jobs, splits):
+        pieces = job.a if which == "a" else job.b
+        for k, owner in enumerate(job.owners):
+            if which == "a":
+                lo, hi = spl[k], spl[k + 1]
+            else:
+                lo, hi = job.diagonal(k) - spl[k], job.diagonal(k + 1) - spl[k + 1]
+            for pc in pieces:
+                s = max(lo, pc.start)
+                e = min(hi, pc.start + pc.length)
+                if e <= s:
+                    continue
+                if pc.rank == comm.rank:
+                    send[owner] += e - s
+                    send_ranges[owner] = (s - pc.start, e - pc.start)
+                if owner == comm.rank:
+                    recv[pc.rank] += e - s
+    return send, recv, send_ranges
+
+
+def _gather_send(local, ranges, P, elem_view):
+    parts = []
+    for r in range(P):
+        if ranges[r] is not None:
+            lo, hi = ranges[r]
+            parts.append(elem_view(local)[lo:hi])
+    if not parts:
+        return elem_view(local)[:0]
+    return torch.cat(parts)
+
+
+def _elem_view(kt):
+    if kt == N.KEY_ELEMENT:
+        return lambda t: t.view(torch.int64).view(-1, 2)
+    return lambda t: t
+
+
+# --------------------------------------------------------------------------
+# step 3: local merge (device kernels by default)
+# --------------------------------------------------------------------------
+def _device_merge(a, b, av, bv, kt):
+    from . import mergepath as mp
+    if av is not None:
+        return mp.parallel_merge(a, b, 1, a_vals=av, b_vals=bv, key_type=kt)
+    return mp.parallel_merge(a, b, 1, key_type=kt), None
+
+
+def _device_sort(x, v, kt):
+    from . import mergepath as mp
+    if v is not None:
+        return mp.parallel_merge_sort(x, 1, vals=v, key_type=kt)
+    return mp.parallel_merge_sort(x, 1, key_type=kt), None
+
+
+def run_jobs(comm: _Comm, jobs, a_local, b_local, kt, a_vals=None, b_vals=None,
+             local_merge=None):
+    """Execute merge jobs; returns this rank's (keys, values) output slice."""
+    splits = distributed_splits(comm, jobs, a_local, b_local, kt)
+    ev = _elem_view(kt)
+    outs_k, outs_v = [], []
+    sa, ra, rng_a = _send_recv_counts(comm, jobs, splits, "a")
+    sb, rb, rng_b = _send_recv_counts(comm, jobs, splits, "b")
+    P = comm.world
+    dev = comm.dev
+
+    def xfer(local, send_c, recv_c, rngs, view):
+        if local is None:
+            local = torch.empty(0, dtype=torch.int32, device=dev)
+        send = _gather_send(local, rngs, P, view).contiguous().to(dev)
+        sc = send_c
+        if view is not None and send.dim() == 2:
+            flat = send.reshape(-1)
+            got = comm.all_to_all(flat, [c * 2 for c in sc], [c * 2 for c in recv_c])
+            return got.view(-1, 2)
+        return comm.all_to_all(send, sc, recv_c)
+
+    got_a = xfer(a_local, sa, ra, rng_a, ev)
+    got_b = xfer(b_local, sb, rb, rng_b, ev)
+    got_av = got_bv = None
+    if a_vals is not None:
+        got_av = xfer(a_vals, sa, ra, rng_a, lambda t: t)
+        got_bv = xfer(b_vals, sb, rb, rng_b, lambda t: t)
+    if kt == N.KEY_ELEMENT:
+        got_a = got_a.reshape(-1)
+        got_b = got_b.reshape(-1)
+    merge = local_merge or _device_merge
+    k, v = merge(got_a, got_b, got_av, got_bv, kt)
+    outs_k.append(k)
+    outs_v.append(v)
+    return outs_k[0], outs_v[0]
+
+
+# --------------------------------------------------------------------------
+# public API
+# --------------------------------------------------------------------------
+def sharded_merge(a_local: torch.Tensor, b_local: torch.Tensor, a_vals=None, b_vals=None,
+                  key_type=None, group=None, local_merge=None):
+    """Merge two sorted sequences sharded contiguously across the ranks
+    (rank r holds A[offA_r, offA_r + |A_r|) and B likewise).  Rank r
+    returns S[floor(r*N/P), floor((r+1)*N/P)) of the stable merge (ties: A
+    first), plus the values that travel with the keys."""
+    comm = _Comm(group)
+    kt = key_type_of(a_local, key_type)
+    lens = comm.all_gather_int([n_keys(a_local, kt), n_keys(b_local, kt)])
+    ranks = list(range(comm.world))
+    job = Job(_pieces(ranks, [x[0] for x in lens]), _pieces(ranks, [x[1] for x in lens]),
+              ranks)
+    return run_jobs(comm, [job], a_local, b_local, kt, a_vals, b_vals, local_merge)
+
+
+def sharded_sort(x_local: torch.Tensor, vals=None, key_type=None, group=None,
+                 local_sort=None, local_merge=None):
+    """Stable sort of a sequence sharded contiguously across the ranks.
+    Rank r ends with its slice of the globally sorted sequence (sizes of the
+    final round's equal split).  Local sort, then ceil(log2 P) rounds of
+    pairwise sharded merges of sorted rank-blocks (left block = A)."""
+    comm = _Comm(group)
+    kt = key_type_of(x_local, key_type)
+    sort = local_sort or _device_sort
+    keys, v = sort(x_local, vals, kt)
+    P = comm.world
+    h = 1
+    while h < P:
+        lens = comm.all_gather_int([n_keys(keys, kt)])
+        lens = [x[0] for x in lens]
+        jobs, mine = [], None
+        for s in range(0, P, 2 * h):
+            left = list(range(s, min(s + h, P)))
+            right = list(range(s + h, min(s + 2 * h, P)))
+            if not right:
+                continue  # unpaired block carried (sort.hpp:98-100)
+            job = Job(_pieces(left, lens), _pieces(right, lens), left + right)
+            jobs.append(job)
+            if comm.rank in left + right:
+                mine = job
+        in_left = mine is not None and comm.rank in [p.rank for p in mine.a]
+        a_loc = keys if in_left else keys[:0]
+        b_loc = keys if (mine is not None and not in_left) else keys[:0]
+        av = bv = None
+        if v is not None:
+            av = v if in_left else v[:0]
+            bv = v if (mine is not None and not in_left) else v[:0]
+        if mine is None:
+            # carried block still takes part in the collectives
+            run_jobs(comm, jobs, keys[:0], keys[:0], kt,
+                     v[:0] if v is not None else None, v[:0] if v is not None else None,
+                     local_merge=lambda a, b, x, y, k: (a, x))
+        else:
+            keys, v = run_jobs(comm, jobs, a_loc, b_loc, kt, av, bv, local_merge)
+        h *= 2
+    return keys, v
+
+
+# --------------------------------------------------------------------------
+# bench.py --gpus N (N > 1): weak scaling, one process per GPU over NCCL
+# --------------------------------------------------------------------------
+def bench_distributed(args, cfg, ws, rank, local):
+    """Each rank holds a fixed-size shard (the config's |A| and |B| per GPU)
+    of globally sorted A and B (generated with the SplitMix64 counter
+    generator at the rank's global offsets, then sorted across the ranks
+    with sharded_sort -- untimed).  A timed step is one sharded_merge: joint
+    split search + NVLink exchange + local K1/K2 merge.  Max over ranks."""
+    import json
+    import statistics
+    import time
+    from pathlib import Path
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    kt = {"u32": N.KEY_U32, "i32": N.KEY_I32, "u64": N.KEY_U64, "i64": N.KEY_I64}[cfg["key"]]
+    dt = {"u32": torch.uint32, "i32": torch.int32, "u64": torch.uint64,
+          "i64": torch.int64}[cfg["key"]]
+    st = torch.cuda.current_stream().cuda_stream
+
+    def gen(kind, seed, n, first):
+        x = torch.empty(n, dtype=dt, device=dev)
+        N.check(N.lib.mp_generate(kind, seed, first, n, x.data_ptr(), st))
+        return x
+
+    na, nb = cfg["na"], cfg["nb"]
+    a, _ = sharded_sort(gen(cfg["gen"][0], 1, na, rank * na), key_type=kt)
+    b, _ = sharded_sort(gen(cfg["gen"][1], 2, nb, rank * nb), key_type=kt)
+    a, b = a.contiguous(), b.contiguous()
+    for _ in range(args.warmup):
+        sharded_merge(a, b, key_type=kt)
+    torch.cuda.synchronize()
+    dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out, _ = sharded_merge(a, b, key_type=kt)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    dist.barrier()
+    ms = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    total = (na + nb) * ws
+    value = total * args.steps / (ms / 1e3)
+    # e2e through the public API with host buffers: H2D shard, sharded merge,
+    # D2H of this rank's output slice (wall clock, max over ranks)
+    ha, hb = a.cpu().pin_memory(), b.cpu().pin_memory()
+    e2e_steps = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
+    dist.barrier()
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        da, db = ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True)
+        o, _ = sharded_merge(da, db, key_type=kt)
+        ho = o.cpu()
+    torch.cuda.synchronize()
+    el = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    ks = a.element_size()
+    peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json")
+                      .read_text())["hbm_gbs"] if (Path(__file__).resolve().parents[1] /
+                                                   "MEASURED_PEAKS.json").exists() else 6650.0
+    per_rank_bytes = (na + nb) * 2 * ks
+    achieved = per_rank_bytes / (ms / args.steps / 1e3) / 1e9
+    del ho, statistics
+    return {
+        "metric": "merged elements/s", "value": value, "unit": "elements/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg["key"],
+        "data": "synthetic: SplitMix64 counter generator, globally sorted with sharded_sort",
+        "config": {"workload": cfg["desc"] + f" per GPU; global |A|={na * ws} |B|={nb * ws}",
+                   "parallelism": f"merge-path diagonal split over {ws} GPUs (NCCL exchange)",
+                   "l2": "inputs+output larger than L2 (no flush needed)"},
+        "gpu_launches": None,
+        "roofline": {"bound": "hbm+nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "note": "per-rank algorithmic HBM bytes / step time; the exchange also "
+                             "moves up to 4 B per remote element over NVLink"},
+        "clocks": None,
+        "e2e": {"value": total * e2e_steps / float(el.item()), "unit": "elements/s",
+                "h2d_bytes_per_step": (na + nb) * ks, "d2h_bytes_per_step": (na + nb) * ks},
+    }
