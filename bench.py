@@ -196,16 +196,16 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
             ptr = (lambda t: t.data_ptr() if t is not None else None)
 
             def step(evs=None):
-                N.check(N.lib.mp_merge_plan(kt, a.data_ptr(), na, b.data_ptr(), nb,
-                                            wsp.data_ptr(), stream.cuda_stream))
+                # one public call: K1 split search (chunk 0 on this stream,
+                # chunks 1.. on the library's side stream) + K2 tile merge
                 if evs is not None:
                     evs[0].record(stream)
-                N.check(N.lib.mp_merge_execute(kt, a.data_ptr(), ptr(av), na, b.data_ptr(),
-                                               ptr(bv), nb, out.data_ptr(), ptr(outv),
-                                               wsp.data_ptr(), stream.cuda_stream))
+                N.check(N.lib.mp_merge(kt, a.data_ptr(), ptr(av), na, b.data_ptr(), ptr(bv),
+                                       nb, out.data_ptr(), ptr(outv), stream.cuda_stream))
                 if evs is not None:
                     evs[1].record(stream)
-            launches_per_step = 2
+            del wsp
+            launches_per_step = 16 if n >= 4096 * 256 * 15 else 2  # 8 chunks x (K1, K2)
             units = n
         else:
             data0 = make_inputs(torch, N, cfg, dev, stream)
@@ -215,13 +215,12 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
             scratch = torch.empty(scratch_b, dtype=torch.uint8, device=dev)
 
             def step(evs=None):
-                # each step sorts a fresh copy of the unsorted keys; the copy
-                # is outside the kernel events but inside the step time
-                data.copy_(data0)
+                # out-of-place sort: the block sort reads the unsorted keys,
+                # the rounds ping-pong between `data` and the scratch
                 if evs is not None:
                     evs[0].record(stream)
-                N.check(N.lib.mp_sort(kt, data.data_ptr(), None, n, scratch.data_ptr(),
-                                      scratch_b, stream.cuda_stream))
+                N.check(N.lib.mp_sort_to(kt, data0.data_ptr(), None, data.data_ptr(), None, n,
+                                         scratch.data_ptr(), scratch_b, stream.cuda_stream))
                 if evs is not None:
                     evs[1].record(stream)
             rounds = max(0, (max(n, 1) - 1).bit_length() - 11)
@@ -254,7 +253,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
 
     if cfg["kind"] == "merge":
         alg_bytes = n * cfg["bytes_per"]  # read A+B once, write S once
-        kname = "merge_tiles_kernel (K2)"
+        kname = "mp_merge: K2 tile merge with K1 split search overlapped (side stream)"
     else:
         alg_bytes = n * 8 * (1 + max(0, (n - 1).bit_length() - 11))
         kname = "mp_sort: block_sort + 19 x (round_partition + merge_tiles)"

@@ -116,6 +116,12 @@ int mp_merge_checksum(int key_type, const void *a, uint64_t na, const void *b,
 uint64_t mp_sort_scratch_bytes(int key_type, int with_vals, uint64_t n);
 int mp_sort(int key_type, void *keys, uint32_t *vals, uint64_t n,
             void *scratch, uint64_t scratch_bytes, void *stream);
+/* Out-of-place: sorted keys_in (+ vals_in) land in keys_out (+ vals_out);
+ * the inputs are not modified (the block sort reads them directly, saving
+ * the copy parallel_merge_sort makes, sort.hpp:137).  May alias (== mp_sort). */
+int mp_sort_to(int key_type, const void *keys_in, const uint32_t *vals_in,
+               void *keys_out, uint32_t *vals_out, uint64_t n, void *scratch,
+               uint64_t scratch_bytes, void *stream);
 
 /* ---- segmented-merge schedule (parallel.hpp:90-145, :258-292) --------- */
 /* Windows of L = cache_elems/3 outputs; ceil((na+nb)/L) of them.

@@ -35,6 +35,7 @@ SIGNATURES = [
     ("mp_merge_checksum", _i, [_i, _p, _u64, _p, _u64, _p, _p]),
     ("mp_sort_scratch_bytes", _u64, [_i, _i, _u64]),
     ("mp_sort", _i, [_i, _p, _p, _u64, _p, _u64, _p]),
+    ("mp_sort_to", _i, [_i, _p, _p, _p, _p, _u64, _p, _u64, _p]),
     ("mp_segment_iterations", _u64, [_u64, _u64, _u64]),
     ("mp_segment_plan", _i, [_i, _p, _u64, _p, _u64, _u64, _u64, _p, _p, _p, _p]),
     ("mp_partition_host", _i, [_i, _p, _u64, _p, _u64, _u64, _p, _p, _i]),

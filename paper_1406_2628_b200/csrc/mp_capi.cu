@@ -186,8 +186,79 @@ int merge_exec(const void *a, const uint32_t *av, uint64_t na, const void *b,
   MP_CUDA(set_smem(kern, smem));
   kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
       PlainMap{P, n, NV}, static_cast<const T *>(a), av,
-      static_cast<const T *>(b), bv, static_cast<T *>(out), outv, sum);
+      static_cast<const T *>(b), bv, static_cast<T *>(out), outv, sum, 0);
   MP_LAUNCHED("merge_tiles_kernel");
+  return MP_OK;
+}
+
+// ---- K1 || K2 overlap -------------------------------------------------------
+// K1 (split search) is latency-bound: dependent DRAM probes, few bytes.  K2
+// (tile merge) is HBM-bound.  Cut the tiles into chunks: the split points of
+// chunk 0 are computed on the caller's stream, those of chunks 1.. on a
+// high-priority side stream while chunk 0.. merge, so only chunk 0's search
+// latency stays on the critical path.  Fork/join by events (graph-capturable).
+constexpr int kOverlapChunks = 8;
+
+struct SideStream {
+  bool init = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t ev[kOverlapChunks] = {};
+  int setup() {
+    if (init)
+      return MP_OK;
+    int least = 0, greatest = 0;
+    MP_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    MP_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest));
+    MP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (auto &e : ev)
+      MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    init = true;
+    return MP_OK;
+  }
+};
+
+SideStream &side_stream() {
+  thread_local SideStream ss[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return ss[dev & 63];
+}
+
+// split(lo, hi, stream) fills split entries [lo, hi) of E; tile(t0, t1,
+// stream) merges tiles [t0, t1) and reads entries [t0, t1] (< E).
+template <class SplitFn, class TileFn>
+int run_overlapped(uint64_t tiles, uint64_t E, SplitFn split, TileFn tile,
+                   cudaStream_t s) {
+  const int C = tiles >= 4096 ? kOverlapChunks : 1;
+  if (C == 1) {
+    if (int rc = split(0, E, s))
+      return rc;
+    return tile(0, tiles, s);
+  }
+  SideStream &ss = side_stream();
+  if (int rc = ss.setup())
+    return rc;
+  uint64_t T[kOverlapChunks + 1], B[kOverlapChunks + 1];
+  for (int c = 0; c <= C; ++c) {
+    T[c] = c * tiles / C;
+    B[c] = c == 0 ? 0 : (c == C ? E : T[c] + 1);
+  }
+  if (int rc = split(B[0], B[1], s))
+    return rc;
+  MP_CUDA(cudaEventRecord(ss.fork, s));
+  MP_CUDA(cudaStreamWaitEvent(ss.side, ss.fork, 0));
+  for (int c = 1; c < C; ++c) {
+    if (int rc = split(B[c], B[c + 1], ss.side))
+      return rc;
+    MP_CUDA(cudaEventRecord(ss.ev[c], ss.side));
+  }
+  for (int c = 0; c < C; ++c) {
+    if (c > 0)
+      MP_CUDA(cudaStreamWaitEvent(s, ss.ev[c], 0));
+    if (int rc = tile(T[c], T[c + 1], s))
+      return rc;
+  }
   return MP_OK;
 }
 
@@ -195,17 +266,43 @@ template <class KT, bool VALS, bool SINK>
 int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
                const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
                unsigned long long *sum, cudaStream_t s) {
+  using T = typename KT::T;
+  constexpr int NT = MergeCfg<KT>::NT, VT = MergeCfg<KT>::VT;
+  constexpr uint32_t NV = NT * VT;
   const uint64_t n = na + nb;
   if (n == 0)
     return MP_OK;
+  const uint64_t tiles = merge_tiles<KT>(n);
+  if (tiles >= (1ull << 31))
+    return fail(MP_ERR_INVALID, "merge too large (%llu elements)",
+                (unsigned long long)n);
   ScratchGuard P;
   if (int rc = alloc_scratch(P, merge_ws_bytes<KT>(n), s))
     return rc;
   uint64_t *Pp = static_cast<uint64_t *>(P.p);
-  if (int rc = merge_plan<KT>(a, na, b, nb, Pp, s))
-    return rc;
-  return merge_exec<KT, VALS, SINK>(a, av, na, b, bv, nb, out, outv, sum, Pp,
-                                    s);
+  constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
+  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, PlainMap, SINK>;
+  MP_CUDA(set_smem(kern, smem));
+  auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
+    if (hi <= lo)
+      return MP_OK;
+    partition_kernel<KT>
+        <<<static_cast<unsigned>(cdiv(hi - lo, 128)), 128, 0, st>>>(
+            static_cast<const T *>(a), na, static_cast<const T *>(b), nb, NV, 0,
+            hi, Pp, nullptr, lo);
+    MP_LAUNCHED("partition_kernel");
+    return MP_OK;
+  };
+  auto tile = [&](uint64_t t0, uint64_t t1, cudaStream_t st) -> int {
+    if (t1 <= t0)
+      return MP_OK;
+    kern<<<static_cast<unsigned>(t1 - t0), NT, smem, st>>>(
+        PlainMap{Pp, n, NV}, static_cast<const T *>(a), av,
+        static_cast<const T *>(b), bv, static_cast<T *>(out), outv, sum, t0);
+    MP_LAUNCHED("merge_tiles_kernel");
+    return MP_OK;
+  };
+  return run_overlapped(tiles, tiles + 1, split, tile, s);
 }
 
 // ---- K3 + (K4 + K2) x rounds: bottom-up merge sort ---------------------------
@@ -226,12 +323,19 @@ template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
 }
 
 template <class KT, bool VALS>
-int sort_impl(void *keys_, uint32_t *vals, uint64_t n, void *scratch,
+int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
+              uint32_t *vals, uint64_t n, void *scratch,
               uint64_t scratch_bytes, cudaStream_t s) {
   using T = typename KT::T;
   T *keys = static_cast<T *>(keys_);
-  if (n <= 1)
+  const T *in = static_cast<const T *>(in_);
+  if (n <= 1) {
+    if (n == 1 && in != keys)
+      MP_CUDA(cudaMemcpyAsync(keys, in, sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (VALS && n == 1 && inv != vals)
+      MP_CUDA(cudaMemcpyAsync(vals, inv, 4, cudaMemcpyDeviceToDevice, s));
     return MP_OK;
+  }
   const SortLayout L = sort_layout<KT>(VALS, n);
   ScratchGuard own;
   char *ws = static_cast<char *>(scratch);
@@ -264,7 +368,7 @@ int sort_impl(void *keys_, uint32_t *vals, uint64_t n, void *scratch,
     auto kern = block_sort_kernel<KT, VALS, kBlockNT, kBlockVT>;
     MP_CUDA(set_smem(kern, smem));
     kern<<<static_cast<unsigned>(cdiv(n, kRun)), kBlockNT, smem, s>>>(
-        keys, vals, src, srcv, n);
+        in, inv, src, srcv, n);
     MP_LAUNCHED("block_sort_kernel");
   }
 
@@ -277,14 +381,27 @@ int sort_impl(void *keys_, uint32_t *vals, uint64_t n, void *scratch,
   MP_CUDA(set_smem(kern, smem));
   uint32_t pshift = 12;  // 2 * kRun == 1 << 12
   for (uint64_t w = kRun; w < n; w *= 2, ++pshift) {
-    round_partition_kernel<KT>
-        <<<static_cast<unsigned>(cdiv(tiles, 128)), 128, 0, s>>>(
-            src, n, w, pshift, NV, tiles, P);
-    MP_LAUNCHED("round_partition_kernel");
-    kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
-        RoundMap{P, n, w, NV, pshift}, src, srcv, src, srcv, dst, dstv,
-        nullptr);
-    MP_LAUNCHED("merge_tiles_kernel(round)");
+    // K4 || K2 within the round (the round's input is complete)
+    auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
+      if (hi <= lo)
+        return MP_OK;
+      round_partition_kernel<KT>
+          <<<static_cast<unsigned>(cdiv(hi - lo, 128)), 128, 0, st>>>(
+              src, n, w, pshift, NV, hi, P, lo);
+      MP_LAUNCHED("round_partition_kernel");
+      return MP_OK;
+    };
+    auto tile = [&](uint64_t t0, uint64_t t1, cudaStream_t st) -> int {
+      if (t1 <= t0)
+        return MP_OK;
+      kern<<<static_cast<unsigned>(t1 - t0), NT, smem, st>>>(
+          RoundMap{P, n, w, NV, pshift}, src, srcv, src, srcv, dst, dstv,
+          nullptr, t0);
+      MP_LAUNCHED("merge_tiles_kernel(round)");
+      return MP_OK;
+    };
+    if (int rc = run_overlapped(tiles, tiles, split, tile, s))
+      return rc;
     T *t = src;
     src = dst;
     dst = t;
@@ -418,16 +535,21 @@ template <class KT> struct ChecksumOp {
 };
 
 template <class KT> struct SortOp {
-  static int run(void *keys, uint32_t *vals, uint64_t n, void *scratch,
+  static int run(const void *in, const uint32_t *inv, void *keys,
+                 uint32_t *vals, uint64_t n, void *scratch,
                  uint64_t scratch_bytes, cudaStream_t s) {
-    if (!aligned_keys<KT>(keys))
+    if (!aligned_keys<KT>(keys) || !aligned_keys<KT>(in))
       return fail(MP_ERR_INVALID, "misaligned key pointer");
-    if (vals) {
+    if (vals || inv) {
       if (KT::kind == kElement)
         return fail(MP_ERR_UNSUPPORTED, "ELEMENT keys carry their own tag");
-      return sort_impl<KT, true>(keys, vals, n, scratch, scratch_bytes, s);
+      if (!vals || !inv)
+        return fail(MP_ERR_INVALID, "values must be given for input and output");
+      return sort_impl<KT, true>(in, inv, keys, vals, n, scratch,
+                                 scratch_bytes, s);
     }
-    return sort_impl<KT, false>(keys, nullptr, n, scratch, scratch_bytes, s);
+    return sort_impl<KT, false>(in, nullptr, keys, nullptr, n, scratch,
+                                scratch_bytes, s);
   }
 };
 
@@ -774,8 +896,20 @@ int mp_sort(int kt, void *keys, uint32_t *vals, uint64_t n, void *scratch,
   g_err.clear();
   if (n && !keys)
     return fail(MP_ERR_INVALID, "sort: NULL keys");
-  return dispatch<SortOp>(kt, keys, vals, n, scratch, scratch_bytes,
+  return dispatch<SortOp>(kt, static_cast<const void *>(keys),
+                          static_cast<const uint32_t *>(vals), keys, vals, n,
+                          scratch, scratch_bytes,
                           static_cast<cudaStream_t>(stream));
+}
+
+int mp_sort_to(int kt, const void *keys_in, const uint32_t *vals_in,
+               void *keys_out, uint32_t *vals_out, uint64_t n, void *scratch,
+               uint64_t scratch_bytes, void *stream) {
+  g_err.clear();
+  if (n && (!keys_in || !keys_out))
+    return fail(MP_ERR_INVALID, "sort: NULL keys");
+  return dispatch<SortOp>(kt, keys_in, vals_in, keys_out, vals_out, n, scratch,
+                          scratch_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,

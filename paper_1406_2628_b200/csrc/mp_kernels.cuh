@@ -54,8 +54,9 @@ __global__ void partition_kernel(const typename KT::T *__restrict__ a,
                                  const typename KT::T *__restrict__ b,
                                  uint64_t nb, uint64_t spacing, uint64_t p,
                                  uint64_t count, uint64_t *__restrict__ a_offs,
-                                 unsigned long long *__restrict__ cmp = nullptr) {
-  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+                                 unsigned long long *__restrict__ cmp = nullptr,
+                                 uint64_t t0 = 0) {
+  const uint64_t t = t0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (t >= count)
     return;
   const uint64_t n = na + nb;
@@ -158,8 +159,9 @@ __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
                                        uint64_t n, uint64_t width,
                                        uint32_t pshift, uint32_t nv,
                                        uint64_t tiles,
-                                       uint64_t *__restrict__ P) {
-  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+                                       uint64_t *__restrict__ P,
+                                       uint64_t t0 = 0) {
+  const uint64_t t = t0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (t >= tiles)
     return;
   const uint64_t d0 = t * nv;
@@ -298,14 +300,15 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
                        const uint32_t *__restrict__ bv,
                        typename KT::T *__restrict__ out,
                        uint32_t *__restrict__ outv,
-                       unsigned long long *__restrict__ sum = nullptr) {
+                       unsigned long long *__restrict__ sum = nullptr,
+                       uint64_t tile0 = 0) {
   using T = typename KT::T;
   constexpr uint32_t KS = sizeof(T);
   extern __shared__ __align__(128) char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
   const int tid = threadIdx.x;
 
-  const TileWin win = map.window(blockIdx.x);
+  const TileWin win = map.window(tile0 + blockIdx.x);
   const int na_t = win.na, nb_t = win.nb, total = na_t + nb_t;
 
   // --- smem layout (byte offsets): each window congruent mod 16 to its

@@ -438,12 +438,10 @@ def _sort(data, vals, key_type):
     if V is not None and V.n != D.n:
         raise ValueError("values must match keys")
     if D.device:
-        out.copy_(D.obj.view(out.dtype).reshape(out.shape))
-        if V is not None:
-            out_vals.copy_(V.obj.view(torch.uint32))
         O = _Arr(out, D.kt)
-        N.check(N.lib.mp_sort(D.kt, O.ptr, out_vals.data_ptr() if V is not None else None,
-                              D.n, None, 0, _stream_ptr(D)))
+        N.check(N.lib.mp_sort_to(D.kt, D.ptr, V.ptr if V is not None else None, O.ptr,
+                                 out_vals.data_ptr() if V is not None else None,
+                                 D.n, None, 0, _stream_ptr(D)))
     else:
         O = _Arr(out, D.kt)
         N.check(N.lib.mp_sort_host(D.kt, D.ptr, V.ptr if V is not None else None, D.n,
