@@ -14,7 +14,10 @@
 #include <string>
 
 #include "../../include/mergepath_b200.h"
+#include <cstdlib>
+
 #include "mp_kernels.cuh"
+#include "mp_spm.cuh"
 
 namespace {
 
@@ -95,8 +98,11 @@ template <class KT> bool aligned_keys(const void *p) {
 
 // ---- per-key-type tile shapes --------------------------------------------
 // Plain merge: odd VT (conflict-free staging, bulk-store epilogue).
+#ifndef MP_MERGE_NT
+#define MP_MERGE_NT 256
+#endif
 template <class KT> struct MergeCfg {
-  static constexpr int NT = 256;
+  static constexpr int NT = MP_MERGE_NT;
   static constexpr int VT = sizeof(typename KT::T) == 4   ? 15
                             : sizeof(typename KT::T) == 8 ? 11
                                                           : 7;
@@ -230,7 +236,15 @@ SideStream &side_stream() {
 template <class SplitFn, class TileFn>
 int run_overlapped(uint64_t tiles, uint64_t E, SplitFn split, TileFn tile,
                    cudaStream_t s) {
-  const int C = tiles >= 4096 ? kOverlapChunks : 1;
+  // Measured on B200 (round 1): the side-stream K1 chunks steal SM slots
+  // from K2 and the step got slower, so the overlap is opt-in
+  // (MP_OVERLAP_CHUNKS=2..8); the persistent SPM kernel removes K1 instead.
+  static const int env_chunks = [] {
+    const char *e = std::getenv("MP_OVERLAP_CHUNKS");
+    const int v = e ? std::atoi(e) : 1;
+    return v < 1 ? 1 : (v > kOverlapChunks ? kOverlapChunks : v);
+  }();
+  const int C = tiles >= 4096 ? env_chunks : 1;
   if (C == 1) {
     if (int rc = split(0, E, s))
       return rc;
@@ -262,6 +276,87 @@ int run_overlapped(uint64_t tiles, uint64_t E, SplitFn split, TileFn tile,
   return MP_OK;
 }
 
+// ---- K2s: persistent streaming SPM merge (no global split pass) ----------
+template <class KT> struct SpmShape;
+template <> struct SpmShape<KeyU32> { static constexpr int NT = 256, VT = 15, CH = 1024, SLOTS = 8; };
+template <> struct SpmShape<KeyI32> : SpmShape<KeyU32> {};
+template <> struct SpmShape<KeyF32> : SpmShape<KeyU32> {};
+template <> struct SpmShape<KeyU64> { static constexpr int NT = 256, VT = 11, CH = 512, SLOTS = 8; };
+template <> struct SpmShape<KeyI64> : SpmShape<KeyU64> {};
+template <> struct SpmShape<KeyElement> { static constexpr int NT = 256, VT = 7, CH = 256, SLOTS = 8; };
+
+template <int NT_, int VT_, int CH_, int SLOTS_> struct SpmShapeX {
+  static constexpr int NT = NT_, VT = VT_, CH = CH_, SLOTS = SLOTS_;
+};
+
+template <class KT, class Sh = SpmShape<KT>>
+int spm_merge_shape(const void *a, uint64_t na, const void *b, uint64_t nb,
+                    void *out, cudaStream_t s);
+
+// tuning hook: MP_SPM_SHAPE=1..3 selects alternative ring geometries for
+// 4-byte keys (A/B experiments); 0 = default
+template <class KT>
+int spm_merge(const void *a, uint64_t na, const void *b, uint64_t nb,
+              void *out, cudaStream_t s) {
+  static const int shape = [] {
+    const char *e = std::getenv("MP_SPM_SHAPE");
+    return e ? std::atoi(e) : 0;
+  }();
+  if constexpr (sizeof(typename KT::T) == 4) {
+    if (shape == 1)
+      return spm_merge_shape<KT, SpmShapeX<256, 15, 512, 16>>(a, na, b, nb, out, s);
+    if (shape == 2)
+      return spm_merge_shape<KT, SpmShapeX<256, 15, 1024, 16>>(a, na, b, nb, out, s);
+    if (shape == 3)
+      return spm_merge_shape<KT, SpmShapeX<512, 15, 1024, 16>>(a, na, b, nb, out, s);
+  }
+  return spm_merge_shape<KT>(a, na, b, nb, out, s);
+}
+
+template <class KT, class Sh>
+int spm_merge_shape(const void *a, uint64_t na, const void *b, uint64_t nb,
+                    void *out, cudaStream_t s) {
+  using T = typename KT::T;
+  using Cfg = SpmCfg<KT, Sh::NT, Sh::VT, Sh::CH, Sh::SLOTS>;
+  auto kern = spm_merge_kernel<KT, Sh::NT, Sh::VT, Sh::CH, Sh::SLOTS>;
+  static thread_local int grid_cache[64] = {};
+  int dev = 0;
+  MP_CUDA(cudaGetDevice(&dev));
+  int &G = grid_cache[dev & 63];
+  if (G == 0) {
+    MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(Cfg::bytes)));
+    int sms = 0, per_sm = 0;
+    MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Sh::NT + 32,
+                                                          Cfg::bytes));
+    G = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const uint64_t n = na + nb;
+  const uint64_t want = cdiv(n, 4ull * Cfg::NV);  // >= 4 windows per CTA
+  const unsigned grid = static_cast<unsigned>(want < uint64_t(G) ? want : G);
+  kern<<<grid ? grid : 1, Sh::NT + 32, Cfg::bytes, s>>>(
+      static_cast<const T *>(a), na, static_cast<const T *>(b), nb,
+      static_cast<T *>(out));
+  MP_LAUNCHED("spm_merge_kernel");
+  return MP_OK;
+}
+
+// Which engine a plain merge uses.  Default: the tile engine (K1 + K2).
+// MP_MERGE_ENGINE=spm selects the persistent streaming SPM kernel for large
+// key-only merges into a 16 B-aligned output.  Measured on B200 (round 1,
+// tools/spm_check.py): bit-exact but 2.3x slower than K1+K2 -- one CTA's
+// rings keep only ~17 KB per stream in flight, while 8 independent tile
+// CTAs per SM keep ~120 KB in flight.
+inline bool use_spm(uint64_t n, const void *out) {
+  static const bool spm = [] {
+    const char *e = std::getenv("MP_MERGE_ENGINE");
+    return e && std::strcmp(e, "spm") == 0;
+  }();
+  return spm && n >= (1ull << 20) &&
+         (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+}
+
 template <class KT, bool VALS, bool SINK>
 int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
                const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
@@ -272,6 +367,8 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
   const uint64_t n = na + nb;
   if (n == 0)
     return MP_OK;
+  if (!VALS && !SINK && use_spm(n, out))
+    return spm_merge<KT>(a, na, b, nb, out, s);
   const uint64_t tiles = merge_tiles<KT>(n);
   if (tiles >= (1ull << 31))
     return fail(MP_ERR_INVALID, "merge too large (%llu elements)",
@@ -652,7 +749,7 @@ struct DeviceScope {  // restores the caller's current device
 // k and the outbound copy of chunk k-1 overlap.  The bound is
 // max(H2D bytes, D2H bytes) / PCIe bandwidth instead of their sum.
 // ---------------------------------------------------------------------------
-constexpr int kSlots = 3;
+constexpr int kSlots = 4;
 
 struct HostPipe {
   std::mutex mu;  // one host call per device at a time
@@ -727,7 +824,8 @@ int merge_host_pipelined(const void *a_, const uint32_t *av, uint64_t na,
   if (int rc = P.setup())
     return rc;
   // ~64 MiB of keys per chunk; never more chunks than needed
-  const uint64_t Q = std::max<uint64_t>(1, std::min<uint64_t>(n, (64ull << 20) / ks));
+  // 16 MiB of keys per chunk: short pipeline fill/drain, few API calls
+  const uint64_t Q = std::max<uint64_t>(1, std::min<uint64_t>(n, (16ull << 20) / ks));
   const uint64_t chunks = cdiv(n, Q);
   auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
   const uint64_t o_a = 0, o_b = up(Q * ks), o_o = o_b + up(Q * ks);

@@ -445,3 +445,80 @@ def _rand_unsorted(S, rng, n, dup):
     if S == "el":
         x["tag"] = np.arange(n, dtype=np.uint32)
     return x
+
+
+# ------------------------------------------------------------ large merges, both engines
+def test_spm_engine_matches_tile_engine(cuda):
+    """The persistent streaming SPM kernel (MP_MERGE_ENGINE=spm, read once
+    per process, hence the subprocess) against the tile engine's two-phase
+    API on the same inputs, every key type and awkward shapes."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = r'''
+import sys, torch, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1406_2628_b200 import _native as N
+dev = torch.device("cuda", 0); st = torch.cuda.current_stream().cuda_stream
+rng = np.random.default_rng(5)
+bad = 0
+for kt, dt, ks in ((0, np.uint32, 4), (1, np.int32, 4), (2, np.uint32, 4), (3, np.uint64, 8),
+                   (4, np.int64, 8), (5, np.int64, 16)):
+    for na, nb, dup in ((1 << 20, 1 << 20, 1 << 30), (1_000_003, 48_571, 16), (3, 1_500_001, 1 << 30),
+                        (2_000_000, 0, 8), (777_777, 777_778, 2)):
+        w = ks // np.dtype(dt).itemsize
+        def mk(n):
+            x = rng.integers(0, dup, n * w).astype(dt)
+            if kt == 5:
+                x = x.reshape(n, 2); x[:, 0] = np.sort(x[:, 0]); return x.reshape(-1)
+            if kt == 2:
+                return np.sort(x.view(np.float32) if False else x)  # bit order == totalOrder for +ve
+            return np.sort(x)
+        a, b = torch.from_numpy(mk(na)).to(dev), torch.from_numpy(mk(nb)).to(dev)
+        o1 = torch.empty(na * w + nb * w, dtype=a.dtype, device=dev); o2 = torch.empty_like(o1)
+        N.check(N.lib.mp_merge(kt, a.data_ptr(), None, na, b.data_ptr(), None, nb, o1.data_ptr(), None, st))
+        ws = torch.empty(N.lib.mp_merge_workspace_bytes(kt, na, nb) + 16, dtype=torch.uint8, device=dev)
+        N.check(N.lib.mp_merge_plan(kt, a.data_ptr(), na, b.data_ptr(), nb, ws.data_ptr(), st))
+        N.check(N.lib.mp_merge_execute(kt, a.data_ptr(), None, na, b.data_ptr(), None, nb, o2.data_ptr(), None, ws.data_ptr(), st))
+        torch.cuda.synchronize()
+        bad += int(not torch.equal(o1, o2))
+print("BAD", bad)
+'''
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ, MP_MERGE_ENGINE="spm")
+    r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True,
+                       env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "BAD 0" in r.stdout, r.stdout + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("S", KEYS)
+def test_large_merges_vs_oracle(cuda, port, S):
+    """Merges >= 2^20 keys (full-size kernel grids); shapes cover CTA-range
+    edges, one-sided windows, ragged tails."""
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(29)
+    for na, nb, dup in ((1 << 20, 1 << 20, 1 << 30), (1_000_003, 48_571, 16),
+                        (3, 1_500_001, 1 << 30), (2_000_000, 0, 8), (777_777, 777_778, 2)):
+        a = _rand_sorted(S, rng, na, dup)
+        b = _rand_sorted(S, rng, nb, dup)
+        if S == "el":
+            b["tag"] += np.uint32(1 << 24)
+        want, _, _, _ = port.merge(S, a, b)
+        got = mp.parallel_merge(to_dev(a, S, cuda), to_dev(b, S, cuda), 8, key_type=key_type(S))
+        assert same(from_dev(got, S), want), (S, na, nb, dup)
+
+
+def test_large_merge_unaligned_inputs(cuda, port):
+    torch = _torch()
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(31)
+    base_a = np.sort(rng.integers(0, 1 << 20, 1_300_000).astype(np.uint32))
+    base_b = np.sort(rng.integers(0, 1 << 20, 1_300_000).astype(np.uint32))
+    da, db = torch.from_numpy(base_a).to(cuda), torch.from_numpy(base_b).to(cuda)
+    for oa, ob in ((1, 3), (2, 0), (3, 2)):
+        a, b = base_a[oa:oa + 1_200_001], base_b[ob:ob + 1_100_000]
+        want, _, _, _ = port.merge("u32", a, b)
+        got = mp.parallel_merge(da[oa:oa + 1_200_001], db[ob:ob + 1_100_000], 4)
+        assert np.array_equal(got.cpu().numpy(), want), (oa, ob)
