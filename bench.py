@@ -196,8 +196,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
             ptr = (lambda t: t.data_ptr() if t is not None else None)
 
             def step(evs=None):
-                # one public call: K1 split search (chunk 0 on this stream,
-                # chunks 1.. on the library's side stream) + K2 tile merge
+                # one public call: K1 split search + K2 tile merge
                 if evs is not None:
                     evs[0].record(stream)
                 N.check(N.lib.mp_merge(kt, a.data_ptr(), ptr(av), na, b.data_ptr(), ptr(bv),
@@ -205,7 +204,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
                 if evs is not None:
                     evs[1].record(stream)
             del wsp
-            launches_per_step = 16 if n >= 4096 * 256 * 15 else 2  # 8 chunks x (K1, K2)
+            launches_per_step = 2  # K1 + K2
             units = n
         else:
             data0 = make_inputs(torch, N, cfg, dev, stream)
@@ -253,7 +252,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
 
     if cfg["kind"] == "merge":
         alg_bytes = n * cfg["bytes_per"]  # read A+B once, write S once
-        kname = "mp_merge: K2 tile merge with K1 split search overlapped (side stream)"
+        kname = "mp_merge step: K1 grid-snapped split search + K2 tile merge"
     else:
         alg_bytes = n * 8 * (1 + max(0, (n - 1).bit_length() - 11))
         kname = "mp_sort: block_sort + 19 x (round_partition + merge_tiles)"

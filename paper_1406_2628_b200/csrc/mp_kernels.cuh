@@ -46,6 +46,52 @@ __device__ __forceinline__ uint64_t diag_search_global(
   return lo;
 }
 
+// The same search with the top levels snapped to a shared grid (every
+// GRID-th element of A and B).  A probe at a grid position mid is decided
+// from the two grid neighbours of B[d-1-mid] when they bracket A[mid]
+// conclusively (Bhi < A[mid] => move right; Blo >= A[mid] => move down) and
+// by the exact element otherwise, so it is still an exact binary search for
+// the same split.  Grid lines are shared by every thread's search and stay
+// in L2; only the last ~log2(2*GRID) probes are private DRAM sectors.
+// (Measured on B200: the plain search's 139 812 tile searches read 615 MB
+// of DRAM at a 6 % L2 hit rate.)
+template <class KT, uint64_t GRID = 1024>
+__device__ __forceinline__ uint64_t diag_search_grid(
+    const typename KT::T *__restrict__ a, uint64_t na,
+    const typename KT::T *__restrict__ b, uint64_t nb, uint64_t d) {
+  using T = typename KT::T;
+  uint64_t lo = d > nb ? d - nb : 0;
+  uint64_t hi = d < na ? d : na;
+  while (hi - lo > 2 * GRID) {
+    uint64_t mid = (lo + ((hi - lo) >> 1)) & ~(GRID - 1);
+    if (mid <= lo)
+      mid = lo + GRID;  // stays < hi since hi - lo > 2*GRID
+    const uint64_t j = d - 1 - mid;  // B index, in [0, nb)
+    const uint64_t jl = j & ~(GRID - 1);
+    const uint64_t jh = jl + GRID < nb ? jl + GRID : nb - 1;
+    const T x = a[mid];
+    bool right;
+    if (take_b<KT>(b[jh], x))  // B[j] <= B[jh] < A[mid]
+      right = true;
+    else if (!take_b<KT>(b[jl], x))  // B[j] >= B[jl] >= A[mid]
+      right = false;
+    else
+      right = take_b<KT>(b[j], x);
+    if (right)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (take_b<KT>(b[d - 1 - mid], a[mid]))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
 // Point t sits on diagonal min(t*spacing, N) (tile mode, p == 0) or on
 // floor(t*N/p) (p-way mode, core.hpp:90-92).  Writes a_off for t < count.
 template <class KT>
@@ -67,10 +113,14 @@ __global__ void partition_kernel(const typename KT::T *__restrict__ a,
     const unsigned __int128 x = static_cast<unsigned __int128>(t) * spacing;
     d = x < n ? static_cast<uint64_t>(x) : n;
   }
-  uint32_t c = 0;
-  a_offs[t] = diag_search_global<KT>(a, na, b, nb, d, &c);
-  if (cmp && c)  // comparison count of the reference's search (core.hpp:128)
-    atomicAdd(cmp, static_cast<unsigned long long>(c));
+  if (cmp) {  // replay the reference's exact probe sequence to count it
+    uint32_t c = 0;
+    a_offs[t] = diag_search_global<KT>(a, na, b, nb, d, &c);
+    if (c)  // comparison count of the reference's search (core.hpp:128)
+      atomicAdd(cmp, static_cast<unsigned long long>(c));
+  } else {
+    a_offs[t] = diag_search_grid<KT>(a, na, b, nb, d);
+  }
 }
 
 // Arbitrary diagonals (used by the drop-in API for single searches and for
@@ -169,7 +219,7 @@ __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
   const uint64_t la = (n - s) < width ? (n - s) : width;
   const uint64_t rest = n - s - la;
   const uint64_t lb = rest < width ? rest : width;
-  P[t] = diag_search_global<KT>(src + s, la, src + s + la, lb, d0 - s);
+  P[t] = diag_search_grid<KT>(src + s, la, src + s + la, lb, d0 - s);
 }
 
 // ---------------------------------------------------------------------------
