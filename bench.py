@@ -196,14 +196,17 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
             ptr = (lambda t: t.data_ptr() if t is not None else None)
 
             def step(evs=None):
-                # one public call: K1 split search + K2 tile merge
+                # mp_merge == mp_merge_plan (K1) + mp_merge_execute (K2); the
+                # two-phase form lets the events isolate K2 for the roofline
+                N.check(N.lib.mp_merge_plan(kt, a.data_ptr(), na, b.data_ptr(), nb,
+                                            wsp.data_ptr(), stream.cuda_stream))
                 if evs is not None:
                     evs[0].record(stream)
-                N.check(N.lib.mp_merge(kt, a.data_ptr(), ptr(av), na, b.data_ptr(), ptr(bv),
-                                       nb, out.data_ptr(), ptr(outv), stream.cuda_stream))
+                N.check(N.lib.mp_merge_execute(kt, a.data_ptr(), ptr(av), na, b.data_ptr(),
+                                               ptr(bv), nb, out.data_ptr(), ptr(outv),
+                                               wsp.data_ptr(), stream.cuda_stream))
                 if evs is not None:
                     evs[1].record(stream)
-            del wsp
             launches_per_step = 2  # K1 + K2
             units = n
         else:
@@ -252,7 +255,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
 
     if cfg["kind"] == "merge":
         alg_bytes = n * cfg["bytes_per"]  # read A+B once, write S once
-        kname = "mp_merge step: K1 grid-snapped split search + K2 tile merge"
+        kname = "merge_tiles_kernel (K2); step = K1 grid-snapped split search + K2"
     else:
         alg_bytes = n * 8 * (1 + max(0, (n - 1).bit_length() - 11))
         kname = "mp_sort: block_sort + 19 x (round_partition + merge_tiles)"
