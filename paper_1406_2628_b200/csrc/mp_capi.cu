@@ -101,10 +101,18 @@ template <class KT> bool aligned_keys(const void *p) {
 #ifndef MP_MERGE_NT
 #define MP_MERGE_NT 256
 #endif
+// B200 A/B (tools/merge_variants.py, ms): VT4 15 -> 23: config 2 0.672 ->
+// 0.666, random u32 2^28+2^28 0.784 -> 0.713; VT8 11 beats 15 on config 3a.
+#ifndef MP_MERGE_VT4
+#define MP_MERGE_VT4 23
+#endif
+#ifndef MP_MERGE_VT8
+#define MP_MERGE_VT8 11
+#endif
 template <class KT> struct MergeCfg {
   static constexpr int NT = MP_MERGE_NT;
-  static constexpr int VT = sizeof(typename KT::T) == 4   ? 15
-                            : sizeof(typename KT::T) == 8 ? 11
+  static constexpr int VT = sizeof(typename KT::T) == 4   ? MP_MERGE_VT4
+                            : sizeof(typename KT::T) == 8 ? MP_MERGE_VT8
                                                           : 7;
 };
 // Sort rounds: the tile (TILE outputs) must divide 2 * 2048 (block-sort run
@@ -115,7 +123,10 @@ template <class KT> struct SortMergeCfg {
   static constexpr int TILE = sizeof(typename KT::T) == 4   ? 4096
                               : sizeof(typename KT::T) == 8 ? 2048
                                                             : 1024;
-  static constexpr int VT = sizeof(typename KT::T) == 4   ? 15
+#ifndef MP_SORT_VT4
+#define MP_SORT_VT4 23  // B200 A/B (tools/sort_variants.py): 15 38.1 ms,
+#endif                  // 19 39.4, 23 35.9, 31 41.3 for 2^30 u32 keys
+  static constexpr int VT = sizeof(typename KT::T) == 4   ? MP_SORT_VT4
                             : sizeof(typename KT::T) == 8 ? 11
                                                           : 7;
   static constexpr int NT = ((TILE + VT - 1) / VT + 31) / 32 * 32;

@@ -245,7 +245,8 @@ __host__ __device__ constexpr uint32_t merge_smem_bytes() {
   using T = typename KT::T;
   constexpr uint32_t NV = NT * VT;
   constexpr uint32_t in_bytes =
-      NV * sizeof(T) + 48 + (VALS ? NV * 4 + 48 : 0);
+      // windows + alignment gaps + one element of read slack per window
+      NV * sizeof(T) + 96 + (VALS ? NV * 4 + 64 : 0);
   constexpr uint32_t st_bytes =
       stage_elems<NT, VT>() * sizeof(T) + 16 +
       (VALS ? stage_elems<NT, VT>() * 4 + 16 : 0);
@@ -320,6 +321,63 @@ __device__ __forceinline__ uint64_t key_of(const Element &x) {
 template <class T>
 __device__ __forceinline__ T lds(const char *smem, uint32_t off) {
   return *reinterpret_cast<const T *>(smem + off);
+}
+
+// Serial stable merge of VT outputs from split (i, j) of the smem windows
+// A = [oA, oA + na*KS), B = [oB, oB + nb*KS) (core.hpp:166-176; ties to A).
+// Branch-free: one predicated choice and ONE smem load (the consumed side's
+// next element) per output.  Fast path: when neither window can run out
+// within VT steps (i + VT <= na and j + VT <= nb -- all but the threads at a
+// window's end) the bounds tests vanish and the cursors are byte offsets
+// (~8 instructions per output).  Loads may touch one element past a window
+// (into the next window or the slack) and are then never used.
+template <class KT, int VT, bool VALS>
+__device__ __forceinline__ void serial_merge(const char *smem, uint32_t oA,
+                                             int na, uint32_t oB, int nb,
+                                             uint32_t oAv, uint32_t oBv, int i,
+                                             int j, typename KT::T (&keys)[VT],
+                                             uint32_t (&vals)[VT]) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  uint32_t pa = oA + i * KS, pb = oB + j * KS;
+  uint32_t pva = oAv + i * 4u, pvb = oBv + j * 4u;
+  if (i + VT <= na && j + VT <= nb) {
+    T ka = lds<T>(smem, pa), kb = lds<T>(smem, pb);
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+      const bool tb = take_b<KT>(kb, ka);
+      keys[k] = tb ? kb : ka;
+      if constexpr (VALS) {
+        vals[k] = lds<uint32_t>(smem, tb ? pvb : pva);
+        pva += tb ? 0u : 4u;
+        pvb += tb ? 4u : 0u;
+      }
+      pa += tb ? 0u : KS;
+      pb += tb ? KS : 0u;
+      const T nxt = lds<T>(smem, tb ? pb : pa);
+      kb = tb ? nxt : kb;
+      ka = tb ? ka : nxt;
+    }
+    return;
+  }
+  const uint32_t ea = oA + na * KS, eb = oB + nb * KS;
+  const uint32_t eva = oAv + na * 4u, evb = oBv + nb * 4u;
+  T ka = lds<T>(smem, min(pa, ea)), kb = lds<T>(smem, min(pb, eb));
+#pragma unroll
+  for (int k = 0; k < VT; ++k) {
+    const bool tb = (pb < eb) && ((pa >= ea) || take_b<KT>(kb, ka));
+    keys[k] = tb ? kb : ka;
+    if constexpr (VALS) {
+      vals[k] = lds<uint32_t>(smem, tb ? min(pvb, evb) : min(pva, eva));
+      pva += tb ? 0u : 4u;
+      pvb += tb ? 4u : 0u;
+    }
+    pa += tb ? 0u : KS;
+    pb += tb ? KS : 0u;
+    const T nxt = lds<T>(smem, tb ? min(pb, eb) : min(pa, ea));
+    kb = tb ? nxt : kb;
+    ka = tb ? ka : nxt;
+  }
 }
 
 // SINK = the register-sink mode (parallel.hpp:181-198): nothing is stored;
@@ -438,21 +496,8 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
   //     (into the next window or the slack) but are never used. ---
   T keys[VT];
   uint32_t vals[VT];
-  T ka = lds<T>(smem, oA + min(i, na_t) * KS);
-  T kb = lds<T>(smem, oB + min(j, nb_t) * KS);
-#pragma unroll
-  for (int k = 0; k < VT; ++k) {
-    const bool tb = (j < nb_t) && ((i >= na_t) || take_b<KT>(kb, ka));
-    keys[k] = tb ? kb : ka;
-    if constexpr (VALS)
-      vals[k] = lds<uint32_t>(smem, tb ? oBv + min(j, nb_t) * 4u
-                                       : oAv + min(i, na_t) * 4u);
-    i += tb ? 0 : 1;
-    j += tb ? 1 : 0;
-    const T nxt = lds<T>(smem, tb ? oB + min(j, nb_t) * KS : oA + min(i, na_t) * KS);
-    kb = tb ? nxt : kb;
-    ka = tb ? ka : nxt;
-  }
+  serial_merge<KT, VT, VALS>(smem, oA, na_t, oB, nb_t, oAv, oBv, i, j, keys,
+                             vals);
   if constexpr (SINK) {
     unsigned long long acc = 0;
 #pragma unroll
@@ -531,7 +576,8 @@ template <class KT, bool VALS, int NT, int VT>
 __host__ __device__ constexpr uint32_t block_sort_smem_bytes() {
   using T = typename KT::T;
   constexpr uint32_t E = NT * VT + (NT * VT) / 32;
-  return ((E * sizeof(T) + 15) & ~15u) + (VALS ? E * 4 : 0);
+  // + one element of read slack past each array (fast merge path)
+  return ((E * sizeof(T) + 15) & ~15u) + (VALS ? E * 4 : 0) + 64;
 }
 
 template <class KT>
@@ -642,19 +688,23 @@ __global__ void __launch_bounds__(NT, (block_sort_min_blocks<KT, VALS, NT>()))
         lo = mid + 1;
     }
     int i = lo, j = diag - lo;
-    T ka = sk(A0 + min(i, width - 1));
-    T kb = sk(B0 + min(j, width - 1));
+    // (a bounds-free fast path like serial_merge's was measured slower here:
+    //  the two unrolled copies cost registers and issue slots)
+    {
+      T ka = sk(A0 + min(i, width - 1));
+      T kb = sk(B0 + min(j, width - 1));
 #pragma unroll
-    for (int k = 0; k < VT; ++k) {
-      const bool tb = (j < width) && ((i >= width) || take_b<KT>(kb, ka));
-      x[k] = tb ? kb : ka;
-      if constexpr (VALS)
-        v[k] = sv(tb ? B0 + j : A0 + i);
-      i += tb ? 0 : 1;
-      j += tb ? 1 : 0;
-      const T nxt = sk(tb ? B0 + min(j, width - 1) : A0 + min(i, width - 1));
-      kb = tb ? nxt : kb;
-      ka = tb ? ka : nxt;
+      for (int k = 0; k < VT; ++k) {
+        const bool tb = (j < width) && ((i >= width) || take_b<KT>(kb, ka));
+        x[k] = tb ? kb : ka;
+        if constexpr (VALS)
+          v[k] = sv(tb ? B0 + j : A0 + i);
+        i += tb ? 0 : 1;
+        j += tb ? 1 : 0;
+        const T nxt = sk(tb ? B0 + min(j, width - 1) : A0 + min(i, width - 1));
+        kb = tb ? nxt : kb;
+        ka = tb ? ka : nxt;
+      }
     }
   }
 
