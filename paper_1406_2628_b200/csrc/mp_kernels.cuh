@@ -387,7 +387,8 @@ __device__ __forceinline__ void serial_merge(const char *smem, uint32_t oA,
 // keys up to 8 B; 3/4 of it when values or 16-byte elements ride along.
 template <class KT, bool VALS, int NT, bool SINK = false>
 constexpr int merge_min_blocks() {
-  return (VALS || SINK)                             ? 1280 / NT
+  return (VALS && sizeof(typename KT::T) == 4)      ? 1024 / NT
+         : (VALS || SINK)                           ? 1280 / NT
          : sizeof(typename KT::T) == 4 && KT::kind != kF32 ? 2048 / NT
          : sizeof(typename KT::T) <= 8               ? 1536 / NT
                                                      : 1280 / NT;
