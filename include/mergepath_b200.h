@@ -160,6 +160,35 @@ int mp_merge_checksum_host(int key_type, const void *a, uint64_t na,
                            const void *b, uint64_t nb, uint64_t *sum,
                            int device);
 
+/* ---- multi-GPU: merging sharded sequences over NVLink ----------------- */
+/* One contiguous piece (shard) of a sorted sequence; keys (and optional
+ * values) are device pointers, possibly peer-mapped memory of another GPU
+ * (mp_ipc_import). */
+typedef struct mp_piece {
+  const void *keys;
+  const uint32_t *vals;
+  uint64_t len;
+} mp_piece;
+
+/* out[0, out_end - out_begin) = positions [out_begin, out_end) of the stable
+ * merge of A = a[0] ++ a[1] ++ ... and B = b[0] ++ ... (1..16 pieces each).
+ * The output range is cut where the merge path crosses piece boundaries
+ * (found by a device probe over the pieces, then one host sync), and each
+ * segment is merged by K1 + K2 directly from the piece pointers: remote
+ * pieces are read over NVLink inside the tile loads (no staging copy).
+ * out_vals non-NULL => every non-empty piece must carry vals. */
+int mp_merge_pieces(int key_type, const mp_piece *a, int na_pieces,
+                    const mp_piece *b, int nb_pieces, uint64_t out_begin,
+                    uint64_t out_end, void *out, uint32_t *out_vals,
+                    void *stream);
+
+/* CUDA IPC for shards owned by other processes: export writes a 64-byte
+ * handle of the allocation holding dev_ptr plus dev_ptr's offset in it;
+ * import maps it (once per allocation, peer access enabled lazily) and
+ * returns the mapped address of the same byte. */
+int mp_ipc_export(const void *dev_ptr, void *handle64, uint64_t *offset);
+int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr);
+
 /* ---- synthetic inputs (bench/tests; SURVEY.md §8d generator) ---------- */
 /* out[k] = config key kind `gen_kind` at global index first+k for `seed`:
  * 0 u32 = x>>32; 1 i32 in [0,1024) = x>>54; 2 u64 = x; 3 u64 < 2^40;

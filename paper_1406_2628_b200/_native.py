@@ -44,6 +44,9 @@ SIGNATURES = [
     ("mp_merge_host", _i, [_i, _p, _p, _u64, _p, _p, _u64, _p, _p, _i]),
     ("mp_sort_host", _i, [_i, _p, _p, _u64, _p, _p, _i]),
     ("mp_merge_checksum_host", _i, [_i, _p, _u64, _p, _u64, _p, _i]),
+    ("mp_merge_pieces", _i, [_i, _p, _i, _p, _i, _u64, _u64, _p, _p, _p]),
+    ("mp_ipc_export", _i, [_p, _p, _p]),
+    ("mp_ipc_import", _i, [_p, _u64, _p]),
     ("mp_generate", _i, [_i, _u64, _u64, _u64, _p, _p]),
 ]
 
@@ -82,3 +85,16 @@ def check(status: int) -> None:
     if status == MP_ERR_INVALID:
         raise ValueError(msg)
     raise MergePathError(status, msg)
+
+
+class Piece(C.Structure):
+    """mp_piece: one contiguous (possibly peer-mapped) shard."""
+    _fields_ = [("keys", C.c_void_p), ("vals", C.c_void_p), ("len", C.c_uint64)]
+
+
+def pieces_array(pieces):
+    """[(keys_ptr, vals_ptr_or_None, len)] -> ctypes mp_piece array."""
+    arr = (Piece * max(1, len(pieces)))()
+    for k, (kp, vp, n) in enumerate(pieces):
+        arr[k].keys, arr[k].vals, arr[k].len = kp, vp, n
+    return arr

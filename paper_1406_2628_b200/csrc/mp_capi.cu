@@ -20,6 +20,7 @@
 
 #include "mp_kernels.cuh"
 #include "mp_spm.cuh"
+#include "mp_pieces.cuh"
 
 namespace {
 
@@ -703,6 +704,99 @@ template <class KT> struct SegmentOp {
   }
 };
 
+// Merge of piece-concatenated sequences (mp_pieces.cuh): probe the piece
+// crossings on the device, cut the output range there, and run the plain
+// K1 + K2 merge on every segment straight from the (peer) piece pointers.
+template <class KT> struct PiecesOp {
+  static int run(const mp_piece *pa, int npa, const mp_piece *pb, int npb,
+                 uint64_t o0, uint64_t o1, void *out_, uint32_t *outv,
+                 cudaStream_t s) {
+    using T = typename KT::T;
+    if (npa < 1 || npb < 1 || npa > kMaxPieces || npb > kMaxPieces)
+      return fail(MP_ERR_INVALID, "merge_pieces: 1..%d pieces per input", kMaxPieces);
+    VPieces A{}, B{};
+    A.n = npa;
+    B.n = npb;
+    bool vals = outv != nullptr;
+    A.start[0] = B.start[0] = 0;
+    for (int k = 0; k < npa; ++k) {
+      A.ptr[k] = pa[k].keys;
+      A.start[k + 1] = A.start[k] + pa[k].len;
+      if (pa[k].len && (!pa[k].keys || !aligned_keys<KT>(pa[k].keys) ||
+                        (vals && !pa[k].vals)))
+        return fail(MP_ERR_INVALID, "merge_pieces: bad A piece %d", k);
+    }
+    for (int k = 0; k < npb; ++k) {
+      B.ptr[k] = pb[k].keys;
+      B.start[k + 1] = B.start[k] + pb[k].len;
+      if (pb[k].len && (!pb[k].keys || !aligned_keys<KT>(pb[k].keys) ||
+                        (vals && !pb[k].vals)))
+        return fail(MP_ERR_INVALID, "merge_pieces: bad B piece %d", k);
+    }
+    const uint64_t na = A.start[npa], nb = B.start[npb];
+    if (o0 > o1 || o1 > na + nb)
+      return fail(MP_ERR_INVALID, "merge_pieces: output range out of bounds");
+    if (o0 == o1)
+      return MP_OK;
+    if (KT::kind == kElement && vals)
+      return fail(MP_ERR_UNSUPPORTED, "ELEMENT keys carry their own tag");
+    // ---- probe: range ends + every piece crossing ----
+    const int probes = 2 + (npa - 1) + (npb - 1);
+    ScratchGuard g;
+    if (int rc = alloc_scratch(g, probes * 16, s))
+      return rc;
+    uint64_t *dprobe = static_cast<uint64_t *>(g.p);
+    pieces_probe_kernel<KT><<<1, 64, 0, s>>>(A, B, o0, o1, dprobe);
+    MP_LAUNCHED("pieces_probe_kernel");
+    std::vector<uint64_t> h(2 * probes);
+    MP_CUDA(cudaMemcpyAsync(h.data(), dprobe, h.size() * 8,
+                            cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    // ---- cut points on the path, sorted by diagonal ----
+    std::vector<std::pair<uint64_t, uint64_t>> pts;  // (a, b)
+    pts.push_back({h[0], h[1]});
+    for (int t = 2; t < probes; ++t) {
+      const uint64_t a = h[2 * t], b = h[2 * t + 1];
+      if (a + b > o0 && a + b < o1)
+        pts.push_back({a, b});
+    }
+    pts.push_back({h[2], h[3]});
+    std::sort(pts.begin(), pts.end(), [](const auto &x, const auto &y) {
+      return x.first + x.second < y.first + y.second;
+    });
+    auto piece_of = [](const VPieces &v, uint64_t i) {
+      int k = 0;
+      while (k + 1 < v.n && i >= v.start[k + 1])
+        ++k;
+      return k;
+    };
+    T *out = static_cast<T *>(out_);
+    for (size_t q = 0; q + 1 < pts.size(); ++q) {
+      const uint64_t a0 = pts[q].first, b0 = pts[q].second;
+      const uint64_t a1 = pts[q + 1].first, b1 = pts[q + 1].second;
+      if (a0 + b0 == a1 + b1)
+        continue;
+      const int ka = piece_of(A, a0), kb = piece_of(B, b0);
+      const T *ap = static_cast<const T *>(A.ptr[ka]) + (a0 - A.start[ka]);
+      const T *bp = static_cast<const T *>(B.ptr[kb]) + (b0 - B.start[kb]);
+      const uint64_t ob = a0 + b0 - o0;
+      int rc;
+      if (vals)
+        rc = merge_impl<KT, true, false>(
+            ap, pa[ka].vals + (a0 - A.start[ka]), a1 - a0, bp,
+            pb[kb].vals + (b0 - B.start[kb]), b1 - b0, out + ob, outv + ob,
+            nullptr, s);
+      else
+        rc = merge_impl<KT, false, false>(ap, nullptr, a1 - a0, bp, nullptr,
+                                          b1 - b0, out + ob, nullptr, nullptr,
+                                          s);
+      if (rc)
+        return rc;
+    }
+    return MP_OK;
+  }
+};
+
 template <class KT> struct ScratchOp {
   static int run(bool vals, uint64_t n, uint64_t *out) {
     *out = n <= 1 ? 0 : sort_layout<KT>(vals, n).total;
@@ -1054,6 +1148,69 @@ int mp_sort_to(int kt, const void *keys_in, const uint32_t *vals_in,
     return fail(MP_ERR_INVALID, "sort: NULL keys");
   return dispatch<SortOp>(kt, keys_in, vals_in, keys_out, vals_out, n, scratch,
                           scratch_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int mp_merge_pieces(int kt, const mp_piece *a, int na_pieces,
+                    const mp_piece *b, int nb_pieces, uint64_t out_begin,
+                    uint64_t out_end, void *out, uint32_t *out_vals,
+                    void *stream) {
+  g_err.clear();
+  if (!a || !b || ((out_end > out_begin) && !out))
+    return fail(MP_ERR_INVALID, "merge_pieces: NULL array");
+  return dispatch<PiecesOp>(kt, a, na_pieces, b, nb_pieces, out_begin, out_end,
+                            out, out_vals, static_cast<cudaStream_t>(stream));
+}
+
+// ---- CUDA IPC (shards of other processes / GPUs) ---------------------------
+int mp_ipc_export(const void *dev_ptr, void *handle64, uint64_t *offset) {
+  g_err.clear();
+  if (!dev_ptr || !handle64 || !offset)
+    return fail(MP_ERR_INVALID, "ipc_export: NULL argument");
+  // base of the allocation containing dev_ptr: cuMemGetAddressRange via the
+  // runtime's driver entry point (no link-time dependency on libcuda)
+  using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+  static GetRange get_range = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault,
+                                &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<GetRange>(fn);
+  }();
+  if (!get_range)
+    return fail(MP_ERR_CUDA, "ipc_export: cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+    return fail(MP_ERR_INVALID, "ipc_export: not a device allocation");
+  cudaIpcMemHandle_t h;
+  MP_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+  std::memcpy(handle64, &h, sizeof h);
+  *offset = reinterpret_cast<unsigned long long>(dev_ptr) - base;
+  return MP_OK;
+}
+
+int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr) {
+  g_err.clear();
+  if (!handle64 || !dev_ptr)
+    return fail(MP_ERR_INVALID, "ipc_import: NULL argument");
+  static std::mutex mu;
+  static std::vector<std::pair<std::string, void *>> opened;
+  const std::string key(static_cast<const char *>(handle64), sizeof(cudaIpcMemHandle_t));
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &e : opened)
+    if (e.first == key) {
+      *dev_ptr = static_cast<char *>(e.second) + offset;
+      return MP_OK;
+    }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  void *base = nullptr;
+  MP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  opened.push_back({key, base});
+  *dev_ptr = static_cast<char *>(base) + offset;
+  return MP_OK;
 }
 
 int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,

@@ -343,14 +343,109 @@ def run_jobs(comm: _Comm, jobs, a_local, b_local, kt, a_vals=None, b_vals=None,
 
 
 # --------------------------------------------------------------------------
+# fused transport: peer-mapped shards read directly by the merge kernels
+# --------------------------------------------------------------------------
+def _export(t: torch.Tensor):
+    import ctypes as C
+    if t.numel() == 0:
+        return None
+    h = (C.c_char * 64)()
+    off = C.c_uint64(0)
+    N.check(N.lib.mp_ipc_export(t.data_ptr(), h, C.byref(off)))
+    return bytes(h), off.value
+
+
+def _import(rec) -> int:
+    import ctypes as C
+    if rec is None:
+        return 0
+    handle, off = rec
+    p = C.c_void_p()
+    buf = C.create_string_buffer(handle, 64)
+    N.check(N.lib.mp_ipc_import(buf, off, C.byref(p)))
+    return p.value or 0
+
+
+class P2PMerger:
+    """Multi-GPU merge with the exchange fused into the merge kernels.
+
+    Every rank exports its A and B shards (CUDA IPC); every rank maps all
+    peers' shards once (peer access over NVLink 5 / NVSwitch) and runs
+    mp_merge_pieces on its output slice S[floor(rN/P), floor((r+1)N/P)):
+    the piece-crossing probe reads peer keys directly and the K1/K2 tile
+    loads pull their windows from peer HBM -- no all_to_all, no staging
+    buffer, one kernel set per rank.  Barriers bracket each merge (inputs
+    complete before anyone reads them; nobody reuses a shard while a peer
+    may still read it)."""
+
+    def __init__(self, a_local, b_local, a_vals=None, b_vals=None, key_type=None,
+                 group=None):
+        self.comm = _Comm(group)
+        self.kt = key_type_of(a_local, key_type)
+        self.a, self.b, self.av, self.bv = a_local, b_local, a_vals, b_vals
+        me = (n_keys(a_local, self.kt), n_keys(b_local, self.kt), _export(a_local),
+              _export(b_local), _export(a_vals) if a_vals is not None else None,
+              _export(b_vals) if b_vals is not None else None)
+        recs = [None] * self.comm.world
+        dist.all_gather_object(recs, me, group=group)
+        self.pa, self.pb = [], []
+        for r, (la, lb, ea, eb, eav, ebv) in enumerate(recs):
+            if r == self.comm.rank:
+                ka, kb = a_local.data_ptr() if la else 0, b_local.data_ptr() if lb else 0
+                va = a_vals.data_ptr() if a_vals is not None and la else None
+                vb = b_vals.data_ptr() if b_vals is not None and lb else None
+            else:
+                ka, kb = _import(ea), _import(eb)
+                va = _import(eav) if eav is not None else None
+                vb = _import(ebv) if ebv is not None else None
+            self.pa.append((ka or None, va, la))
+            self.pb.append((kb or None, vb, lb))
+        self.na = sum(p[2] for p in self.pa)
+        self.nb = sum(p[2] for p in self.pb)
+        n, P, r = self.na + self.nb, self.comm.world, self.comm.rank
+        self.o0, self.o1 = r * n // P, (r + 1) * n // P
+        self._arr_a = N.pieces_array(self.pa)
+        self._arr_b = N.pieces_array(self.pb)
+
+    def __call__(self, out=None, out_vals=None, sync=True):
+        m = self.o1 - self.o0
+        if out is None:
+            out = torch.empty(m * (2 if self.kt == N.KEY_ELEMENT else 1),
+                              dtype=self.a.dtype if self.kt != N.KEY_ELEMENT else torch.int64,
+                              device=self.a.device)
+        if out_vals is None and self.av is not None:
+            out_vals = torch.empty(m, dtype=torch.uint32, device=self.a.device)
+        stream = torch.cuda.current_stream(self.a.device)
+        if sync:
+            stream.synchronize()
+            dist.barrier(group=self.comm.group)
+        N.check(N.lib.mp_merge_pieces(self.kt, self._arr_a, len(self.pa), self._arr_b,
+                                      len(self.pb), self.o0, self.o1, out.data_ptr(),
+                                      out_vals.data_ptr() if out_vals is not None else None,
+                                      stream.cuda_stream))
+        if sync:
+            stream.synchronize()
+            dist.barrier(group=self.comm.group)
+        return out, out_vals
+
+
+# --------------------------------------------------------------------------
 # public API
 # --------------------------------------------------------------------------
 def sharded_merge(a_local: torch.Tensor, b_local: torch.Tensor, a_vals=None, b_vals=None,
-                  key_type=None, group=None, local_merge=None):
+                  key_type=None, group=None, local_merge=None, transport="nccl"):
     """Merge two sorted sequences sharded contiguously across the ranks
     (rank r holds A[offA_r, offA_r + |A_r|) and B likewise).  Rank r
     returns S[floor(r*N/P), floor((r+1)*N/P)) of the stable merge (ties: A
-    first), plus the values that travel with the keys."""
+    first), plus the values that travel with the keys.
+
+    transport="nccl": joint split search + all_to_all exchange + local merge
+    (works on any backend, incl. gloo for the CPU tests).
+    transport="p2p": shards mapped over NVLink (CUDA IPC) and pulled by the
+    merge kernels themselves (P2PMerger); build the merger once to reuse
+    the mappings across calls."""
+    if transport == "p2p":
+        return P2PMerger(a_local, b_local, a_vals, b_vals, key_type, group)()
     comm = _Comm(group)
     kt = key_type_of(a_local, key_type)
     lens = comm.all_gather_int([n_keys(a_local, kt), n_keys(b_local, kt)])
