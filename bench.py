@@ -125,6 +125,10 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # smoke-testing the multi-rank path on a one-GPU box: every rank on one
+    # device (MP_BENCH_DEVICE) with gloo plumbing (MP_BENCH_BACKEND=gloo)
+    if "MP_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["MP_BENCH_DEVICE"])
     return ws, rank, local
 
 
@@ -515,6 +519,9 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-GPU exchange: NVLink pull fused into the merge (p2p) "
+                         "or all_to_all staging (nccl)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -530,7 +537,11 @@ def main(argv=None):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("MP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     if dist_on and cfg["kind"] == "merge":
         from paper_1406_2628_b200.multigpu import bench_distributed
         res = bench_distributed(args, cfg, ws, rank, local)
