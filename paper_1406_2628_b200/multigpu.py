@@ -335,6 +335,15 @@ def run_jobs(comm: _Comm, jobs, a_local, b_local, kt, a_vals=None, b_vals=None,
     if kt == N.KEY_ELEMENT:
         got_a = got_a.reshape(-1)
         got_b = got_b.reshape(-1)
+    if local_merge is None:
+        # exchange buffers live on the backend's device (CPU for gloo);
+        # the local merge runs where the shards live
+        home = next((t.device for t in (a_local, b_local) if t is not None and t.is_cuda),
+                    None)
+        if home is not None:
+            got_a, got_b = got_a.to(home), got_b.to(home)
+            if got_av is not None:
+                got_av, got_bv = got_av.to(home), got_bv.to(home)
     merge = local_merge or _device_merge
     k, v = merge(got_a, got_b, got_av, got_bv, kt)
     outs_k.append(k)
