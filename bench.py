@@ -57,6 +57,9 @@ CONFIGS = {
                desc="config3b: stable merge u64 key + u32 value, |A|=2^29 |B|=2^25, B below A"),
     "4": dict(kind="sort", key="u32", gen=(0, None), n=1 << 30, bytes_per=160,
               desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 2048-key block sort + 19 rounds"),
+    "5": dict(kind="merge", key="f32", gen=(5, 6), na=1 << 31, nb=1 << 31, bytes_per=8,
+              desc="config5: stable merge f32 |A|=|B|=2^31, A~Normal(0,1), B~Exp(1), IEEE "
+                   "totalOrder (one GPU: the whole merge; --gpus 8: sharded)"),
 }
 KT = {"u32": 0, "i32": 1, "f32": 2, "u64": 3, "i64": 4}
 KSIZE = {"u32": 4, "i32": 4, "f32": 4, "u64": 8, "i64": 8}
@@ -308,6 +311,10 @@ def run_e2e(args, cfg, torch, N, dev, local, dist_on, ws):
     with torch.cuda.device(dev):
         if cfg["kind"] == "merge":
             a, b, av, bv = make_inputs(torch, N, cfg, dev, torch.cuda.current_stream())
+            sample = None
+            if a.numel() + b.numel() > (1 << 30):  # host RAM: 2^28-prefixes
+                a, b = a[: 1 << 28].contiguous(), b[: 1 << 28].contiguous()
+                sample = "2^28-element prefixes of A and B (host RAM bound)"
             ha = a.cpu().pin_memory()
             hb = b.cpu().pin_memory()
             n = a.numel() + b.numel()
@@ -348,7 +355,8 @@ def run_e2e(args, cfg, torch, N, dev, local, dist_on, ws):
     del np
     return {"value": n * ws * steps / el, "unit": unit, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps,
-            "api": "mp_merge_host" if cfg["kind"] == "merge" else "mp_sort_host"}
+            "api": "mp_merge_host" if cfg["kind"] == "merge" else "mp_sort_host",
+            **({"sample": sample} if cfg["kind"] == "merge" and sample else {})}
 
 
 # --------------------------------------------------------------------------
@@ -441,13 +449,26 @@ def cpu_baseline(cfg, a, b, out_dev, args):
     if not B.REF_LIB.exists():
         return {"value": None, "unit": None, "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built"}
+    import numpy as np
+    prefix = None
+    if cfg["kind"] == "merge" and a.numel() + b.numel() > (1 << 30):
+        # host-RAM bound: time (and verify) the merge of the 2^27-prefixes
+        prefix = 1 << 27
+        a, b = a[:prefix], b[:prefix]
     ha, hb = ref_inputs_from_device(cfg, a, b)
     frac = None if cfg["kind"] == "merge" else 1 / 16
     val, sec, p, sample, out = time_reference(cfg, ha, hb, reps=5, budget_s=20, sample_frac=frac)
+    if prefix:
+        sample = f"2^27-element prefixes of A and B (host RAM bound); " + sample
     res = {"value": val, "unit": "elements/s" if cfg["kind"] == "merge" else "keys/s",
            "cores": p, "kind": "reference", "sample": sample, "seconds_per_rep": sec}
     if out_dev is not None:  # verify before report (mergebench.cpp:263-265)
+        if prefix:
+            from paper_1406_2628_b200 import mergepath as mp
+            out_dev = mp.parallel_merge(a.contiguous(), b.contiguous(), 1)
         got = out_dev.cpu().numpy()
+        if got.dtype == np.float32:
+            got = got.view(np.uint32)
         want = out["key"] if cfg.get("vals") else out
         res["gpu_output_bit_exact_vs_reference"] = bool(got.tobytes() == want.tobytes())
     return res

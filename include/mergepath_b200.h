@@ -192,7 +192,11 @@ int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr);
 /* ---- synthetic inputs (bench/tests; SURVEY.md §8d generator) ---------- */
 /* out[k] = config key kind `gen_kind` at global index first+k for `seed`:
  * 0 u32 = x>>32; 1 i32 in [0,1024) = x>>54; 2 u64 = x; 3 u64 < 2^40;
- * 4 u64 in [2^40, 2^64).  x_i = mix64(seed + i*0x9E3779B97F4A7C15). */
+ * 4 u64 in [2^40, 2^64); 5 f32 Normal(0,1) (Box-Muller, cosine branch, in
+ * double); 6 f32 Exp(1).  x_i = mix64(seed + i*0x9E3779B97F4A7C15).
+ * Kinds 5/6 use the device's double-precision log/cospi: bytes can differ in
+ * the last float ulp from a host-libm generator, so parity checks always run
+ * on copies of the same device-generated bytes. */
 int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,
                 void *out, void *stream);
 

@@ -547,6 +547,21 @@ __global__ void generate_kernel(int kind, uint64_t seed, uint64_t first,
     static_cast<unsigned long long *>(out)[k] =
         (1ull << 40) + __umul64hi(x, ~0ull - (1ull << 40) + 1ull);
     break;
+  case 5: {  // Normal(0,1), Box-Muller cosine branch
+    const uint64_t i = first + k;
+    const uint64_t x0 = mix64_dev(seed + (2 * i) * 0x9E3779B97F4A7C15ULL);
+    const uint64_t x1 = mix64_dev(seed + (2 * i + 1) * 0x9E3779B97F4A7C15ULL);
+    const double u1 = static_cast<double>((x0 >> 11) + 1) * 0x1.0p-53;
+    const double u2 = static_cast<double>(x1 >> 11) * 0x1.0p-53;
+    static_cast<float *>(out)[k] =
+        static_cast<float>(sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+    break;
+  }
+  case 6: {  // Exp(1)
+    const double u = static_cast<double>((x >> 11) + 1) * 0x1.0p-53;
+    static_cast<float *>(out)[k] = static_cast<float>(-log(u));
+    break;
+  }
   }
 }
 
@@ -1216,7 +1231,7 @@ int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr) {
 int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,
                 void *out, void *stream) {
   g_err.clear();
-  if (gen_kind < 0 || gen_kind > 4)
+  if (gen_kind < 0 || gen_kind > 6)
     return fail(MP_ERR_INVALID, "generate: unknown kind %d", gen_kind);
   if (n == 0)
     return MP_OK;

@@ -326,6 +326,36 @@ def test_config1_bit_exact_and_partition(cuda, port):
     assert mp.parallel_merge(a, b, 8).tobytes() == want.tobytes()  # host entry
 
 
+def test_config5_shape_totalorder_merge(cuda, port):
+    """Config 5 inputs (f32 Normal(0,1) and Exp(1) from the device generator,
+    sorted by IEEE totalOrder with our sort) at 2^22 + 2^22: the merge of the
+    same bytes equals the oracle's, -0.0/+0.0 included."""
+    torch = _torch()
+    from paper_1406_2628_b200 import _native as N
+    n = 1 << 22
+    st = torch.cuda.current_stream().cuda_stream
+    a = torch.empty(n, dtype=torch.float32, device=cuda)
+    b = torch.empty(n, dtype=torch.float32, device=cuda)
+    N.check(N.lib.mp_generate(5, 1, 0, n, a.data_ptr(), st))
+    N.check(N.lib.mp_generate(6, 2, 0, n, b.data_ptr(), st))
+    a[::97] = -0.0  # signed zeros on both sides
+    b[::89] = 0.0
+    b[1::89] = -0.0
+    for x in (a, b):
+        N.check(N.lib.mp_sort(N.KEY_F32, x.data_ptr(), None, n, None, 0, st))
+    ha = a.cpu().numpy().view(np.uint32)
+    hb = b.cpu().numpy().view(np.uint32)
+    order = lambda u: np.where(u & 0x80000000, ~u, u | 0x80000000)  # noqa: E731
+    assert np.all(np.diff(order(ha).astype(np.int64)) >= 0)
+    af = a.cpu().numpy()
+    assert abs(float(af.mean())) < 0.01 and abs(float(af.std()) - 1) < 0.01
+    assert abs(float(b.cpu().numpy().mean()) - 1) < 0.01
+    from paper_1406_2628_b200 import mergepath as mp
+    got = mp.parallel_merge(a, b, 8)
+    want, _, _, _ = port.merge("f32", ha, hb)
+    assert np.array_equal(got.cpu().numpy().view(np.uint32), want)
+
+
 def _sorted_dev(kind, seed, n, dev):
     torch = _torch()
     from paper_1406_2628_b200 import _native as N
