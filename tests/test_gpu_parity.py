@@ -349,7 +349,7 @@ def test_config5_shape_totalorder_merge(cuda, port):
     assert np.all(np.diff(order(ha).astype(np.int64)) >= 0)
     af = a.cpu().numpy()
     assert abs(float(af.mean())) < 0.01 and abs(float(af.std()) - 1) < 0.01
-    assert abs(float(b.cpu().numpy().mean()) - 1) < 0.01
+    assert abs(float(b.cpu().numpy().mean()) - 1) < 0.05  # 2/89 of B zeroed above
     from paper_1406_2628_b200 import mergepath as mp
     got = mp.parallel_merge(a, b, 8)
     want, _, _, _ = port.merge("f32", ha, hb)
