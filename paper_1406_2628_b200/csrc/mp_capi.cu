@@ -21,6 +21,7 @@
 #include "mp_kernels.cuh"
 #include "mp_spm.cuh"
 #include "mp_pieces.cuh"
+#include "mp_radix.cuh"
 
 namespace {
 
@@ -474,7 +475,28 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   T *dst = in_place ? aux : keys;
   uint32_t *dstv = in_place ? auxv : vals;
 
-  {
+  // MP_BLOCK_SORT=radix: LSD radix block sort for bare 32-bit keys (same
+  // bytes).  Opt-in: measured on B200 at 30.0 ms for 2^30 keys vs 8.3 ms for
+  // the merge-based block sort (match.any ranking + 1.7 G bank conflicts),
+  // though it issues 35 % fewer instructions.
+  static const bool radix_bs = [] {
+    const char *e = std::getenv("MP_BLOCK_SORT");
+    return e && std::strcmp(e, "radix") == 0;
+  }();
+  bool block_sorted = false;
+  if constexpr (!VALS && sizeof(T) == 4 && KT::kind != kElement) {
+    if (radix_bs) {
+      static_assert(kRadixNV == kRun, "radix block = sort run");
+      constexpr uint32_t smem = radix_smem_bytes();
+      auto kern = block_radix_sort_kernel<KT>;
+      MP_CUDA(set_smem(kern, smem));
+      kern<<<static_cast<unsigned>(cdiv(n, kRun)), kRadixNT, smem, s>>>(in, src,
+                                                                       n);
+      MP_LAUNCHED("block_radix_sort_kernel");
+      block_sorted = true;
+    }
+  }
+  if (!block_sorted) {
     constexpr uint32_t smem = block_sort_smem_bytes<KT, VALS, kBlockNT, kBlockVT>();
     auto kern = block_sort_kernel<KT, VALS, kBlockNT, kBlockVT>;
     MP_CUDA(set_smem(kern, smem));
