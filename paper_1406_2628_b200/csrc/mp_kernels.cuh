@@ -689,27 +689,12 @@ __global__ void __launch_bounds__(NT, (block_sort_min_blocks<KT, VALS, NT>()))
         lo = mid + 1;
     }
     int i = lo, j = diag - lo;
-    if (i + VT <= width && j + VT <= width) {
-      // bounds-free fast path (unrolled); a load one past A reads B's first
-      // key, one past B the next group or the slack -- never used
-      T ka = sk(A0 + i), kb = sk(B0 + j);
-#pragma unroll
-      for (int k = 0; k < VT; ++k) {
-        const bool tb = take_b<KT>(kb, ka);
-        x[k] = tb ? kb : ka;
-        if constexpr (VALS)
-          v[k] = sv(tb ? B0 + j : A0 + i);
-        i += tb ? 0 : 1;
-        j += tb ? 1 : 0;
-        const T nxt = sk(tb ? B0 + j : A0 + i);
-        kb = tb ? nxt : kb;
-        ka = tb ? ka : nxt;
-      }
-    } else {
-      // threads at a run's end: bounds-checked, kept rolled (code size)
+    // (a bounds-free fast path like serial_merge's was measured slower here,
+    //  both with an unrolled and with a rolled slow path: 8.3 -> 11.0 ms)
+    {
       T ka = sk(A0 + min(i, width - 1));
       T kb = sk(B0 + min(j, width - 1));
-#pragma unroll 1
+#pragma unroll
       for (int k = 0; k < VT; ++k) {
         const bool tb = (j < width) && ((i >= width) || take_b<KT>(kb, ka));
         x[k] = tb ? kb : ka;
