@@ -566,6 +566,9 @@ def main(argv=None):
     if dist_on and cfg["kind"] == "merge":
         from paper_1406_2628_b200.multigpu import bench_distributed
         res = bench_distributed(args, cfg, ws, rank, local)
+    elif dist_on:
+        from paper_1406_2628_b200.multigpu import bench_distributed_sort
+        res = bench_distributed_sort(args, cfg, ws, rank, local)
     else:
         res = run_ours(args, cfg, ws, rank, local, dist_on)
     if rank == 0:

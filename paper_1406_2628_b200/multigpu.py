@@ -438,6 +438,90 @@ class P2PMerger:
         return out, out_vals
 
 
+class P2PSorter:
+    """Multi-GPU stable merge sort with the exchange fused into the merges.
+
+    Each rank owns two device buffers (ping/pong) of `capacity` keys, mapped
+    into every peer once (CUDA IPC).  run(): local mp_sort of the rank's
+    shard into ping, then ceil(log2 P) rounds; in round r, rank blocks of
+    h = 2^r ranks are paired (left block = A, so the sort stays stable w.r.t.
+    input order; an unpaired last block is carried, sort.hpp:98-100) and
+    every rank of a pair merges its equal slice of the pair's output with
+    mp_merge_pieces straight from the peers' mapped buffers into its pong
+    buffer.  A barrier closes each round (nobody overwrites a buffer a peer
+    may still read), then ping/pong swap.  Slice sizes are computed, not
+    communicated: every rank knows every length."""
+
+    def __init__(self, capacity: int, dtype, key_type: int, group=None, device=None):
+        self.comm = _Comm(group)
+        self.kt = key_type
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        words = capacity * (2 if key_type == N.KEY_ELEMENT else 1)
+        wdt = torch.int64 if key_type == N.KEY_ELEMENT else dtype
+        self.buf = [torch.empty(max(words, 1), dtype=wdt, device=dev) for _ in range(2)]
+        recs = [None] * self.comm.world
+        dist.all_gather_object(recs, (_export(self.buf[0]), _export(self.buf[1])), group=group)
+        self.peer = [[0, 0] for _ in range(self.comm.world)]
+        for r, (e0, e1) in enumerate(recs):
+            if r == self.comm.rank:
+                self.peer[r] = [self.buf[0].data_ptr(), self.buf[1].data_ptr()]
+            else:
+                self.peer[r] = [_import(e0), _import(e1)]
+        self.scratch = None
+
+    def run(self, x_local: torch.Tensor, sync=True):
+        P, me = self.comm.world, self.comm.rank
+        kt = self.kt
+        n_me = n_keys(x_local, kt)
+        lens = [x[0] for x in self.comm.all_gather_int([n_me])]
+        stream = torch.cuda.current_stream(self.buf[0].device)
+        st = stream.cuda_stream
+        sb = N.lib.mp_sort_scratch_bytes(kt, 0, n_me)
+        if self.scratch is None or self.scratch.numel() < max(sb, 16):
+            self.scratch = torch.empty(max(sb, 16), dtype=torch.uint8, device=self.buf[0].device)
+        N.check(N.lib.mp_sort_to(kt, x_local.data_ptr(), None, self.buf[0].data_ptr(), None,
+                                 n_me, self.scratch.data_ptr(), self.scratch.numel(), st))
+        cur, h = 0, 1
+        while h < P:
+            if sync:
+                stream.synchronize()
+                dist.barrier(group=self.comm.group)
+            new_lens = list(lens)
+            s0 = (me // (2 * h)) * 2 * h
+            left = list(range(s0, min(s0 + h, P)))
+            right = list(range(s0 + h, min(s0 + 2 * h, P)))
+            for s in range(0, P, 2 * h):  # every block pair's new slice sizes
+                L = list(range(s, min(s + h, P)))
+                R = list(range(s + h, min(s + 2 * h, P)))
+                if R:
+                    owners = L + R
+                    tot = sum(lens[q] for q in owners)
+                    for k, q in enumerate(owners):
+                        new_lens[q] = (k + 1) * tot // len(owners) - k * tot // len(owners)
+            if right:
+                owners = left + right
+                k = owners.index(me)
+                tot = sum(lens[q] for q in owners)
+                o0, o1 = k * tot // len(owners), (k + 1) * tot // len(owners)
+                pa = N.pieces_array([(self.peer[q][cur] if lens[q] else None, None, lens[q])
+                                     for q in left])
+                pb = N.pieces_array([(self.peer[q][cur] if lens[q] else None, None, lens[q])
+                                     for q in right])
+                N.check(N.lib.mp_merge_pieces(kt, pa, len(left), pb, len(right), o0, o1,
+                                              self.buf[1 - cur].data_ptr(), None, st))
+            else:  # carried block: copy through so every rank sits in `1-cur`
+                words = lens[me] * (2 if kt == N.KEY_ELEMENT else 1)
+                self.buf[1 - cur][:words].copy_(self.buf[cur][:words])
+            lens = new_lens
+            cur = 1 - cur
+            h *= 2
+        if sync:
+            stream.synchronize()
+            dist.barrier(group=self.comm.group)
+        words = lens[me] * (2 if kt == N.KEY_ELEMENT else 1)
+        return self.buf[cur][:words]
+
+
 # --------------------------------------------------------------------------
 # public API
 # --------------------------------------------------------------------------
@@ -607,4 +691,75 @@ def bench_distributed(args, cfg, ws, rank, local):
         "clocks": None,
         "e2e": {"value": total * e2e_steps / float(el.item()), "unit": "elements/s",
                 "h2d_bytes_per_step": (na + nb) * ks, "d2h_bytes_per_step": (na + nb) * ks},
+    }
+
+
+def bench_distributed_sort(args, cfg, ws, rank, local):
+    """bench.py --config 4 --gpus N: strong scaling of the 2^30-key sort
+    (BASELINE config 4: each GPU local-sorts a 1/P shard, then Merge Path
+    rounds across GPUs).  Shard r = keys [r*n/P, (r+1)*n/P) of the seed-4
+    SplitMix64 sequence; a timed step = P2PSorter.run (local sort + log2 P
+    fused NVLink merge rounds), max over ranks."""
+    import os
+    import time
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    shrink = int(os.environ.get("MP_BENCH_SCALE", "0"))
+    n = cfg["n"] >> shrink
+    lo, hi = rank * n // ws, (rank + 1) * n // ws
+    x = torch.empty(hi - lo, dtype=torch.uint32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    N.check(N.lib.mp_generate(cfg["gen"][0], 4, lo, hi - lo, x.data_ptr(), st))
+    sorter = P2PSorter((n + ws - 1) // ws + 1, torch.uint32, N.KEY_U32)
+    for _ in range(args.warmup):
+        sorter.run(x)
+    torch.cuda.synchronize()
+    dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sorter.run(x)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    red_dev = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    ms = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    # e2e: pinned host shard -> device, sort, sorted slice back to the host
+    hx = x.cpu().pin_memory()
+    dist.barrier()
+    t = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
+    for _ in range(e2e_steps):
+        x.copy_(hx, non_blocking=True)
+        o = sorter.run(x)
+        ho = o.cpu()
+    torch.cuda.synchronize()
+    el = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    del ho
+    rounds = max(0, (max(n // ws, 1) - 1).bit_length() - 11)
+    passes = 1 + rounds + (ws - 1).bit_length()
+    return {
+        "metric": "merge-sort keys/s", "value": n * args.steps / (ms / 1e3), "unit": "keys/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic: SplitMix64 counter generator, seed 4",
+        "config": {"workload": cfg["desc"] + f"; {ws} GPUs, 1/{ws} shard each",
+                   "parallelism": f"local sort + {(ws - 1).bit_length()} cross-GPU Merge Path "
+                                  "rounds, NVLink pull fused into the merge (CUDA IPC)",
+                   "l2": "inputs+output larger than L2 (no flush needed)"},
+        "gpu_launches": None,
+        "roofline": {"bound": "hbm+nvlink", "unit": "GB/s",
+                     "achieved": (n // ws) * 8 * passes / (ms / args.steps / 1e3) / 1e9,
+                     "peak": 6554.2, "frac": (n // ws) * 8 * passes / (ms / args.steps / 1e3)
+                     / 1e9 / 6554.2, "traffic": None,
+                     "note": f"per-GPU {passes} passes x 8 B/key over the step time"},
+        "clocks": None,
+        "e2e": {"value": n * e2e_steps / float(el.item()), "unit": "keys/s",
+                "h2d_bytes_per_step": (hi - lo) * 4, "d2h_bytes_per_step": (hi - lo) * 4},
     }

@@ -169,3 +169,55 @@ def test_p2p_merger_two_processes(cuda, port):
     assert np.array_equal(gotv, wantv)
     n = na + nb
     assert len(res[0][0]) // 4 == n // 2
+
+
+def _sort_worker(rank, world, port, sizes, q):
+    try:
+        sys.path.insert(0, str(ROOT))
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1406_2628_b200 import _native as N
+        from paper_1406_2628_b200 import multigpu as mg
+        rng = np.random.default_rng(11)
+        x = rng.integers(0, 1 << 20, sum(sizes)).astype(np.uint32)
+        cut = np.concatenate([[0], np.cumsum(sizes)])
+        xl = torch.from_numpy(x[cut[rank]:cut[rank + 1]].copy()).cuda()
+        s = mg.P2PSorter(max(sizes), torch.uint32, N.KEY_U32)
+        out = s.run(xl)
+        out2 = s.run(xl)  # buffers and mappings reused
+        assert torch.equal(out, out2)
+        q.put((rank, out.cpu().numpy().tobytes(), None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, "ERR", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("sizes", [[700_001, 699_999], [500_000, 20_000, 480_000],
+                                   [300_000, 300_000, 300_000, 300_000]])
+def test_p2p_sorter_processes(cuda, sizes):
+    import torch.multiprocessing as tmp
+    world = len(sizes)
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_sort_worker, args=(r, world, port_no, sizes, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, k, v = q.get(timeout=600)
+        assert k != "ERR", v
+        res[r] = k
+    for p in procs:
+        p.join(timeout=120)
+    rng = np.random.default_rng(11)
+    x = rng.integers(0, 1 << 20, sum(sizes)).astype(np.uint32)
+    got = np.frombuffer(b"".join(res[r] for r in range(world)), dtype=np.uint32)
+    assert np.array_equal(got, np.sort(x))
