@@ -245,6 +245,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
                for _ in range(args.steps)]
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        c0 = N.lib.mp_launch_count()
         with ClockSampler(local) as clk:
             t0.record(stream)
             for i in range(args.steps):
@@ -253,6 +254,9 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
             t1.record(stream)
             stream.synchronize()
         torch.cuda.synchronize()
+        counted = N.lib.mp_launch_count() - c0
+        if counted != launches:
+            raise RuntimeError(f"launch count {counted} != expected {launches}")
         barrier(dist_on)
         ms = t0.elapsed_time(t1)
         kern_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in evs)
@@ -565,10 +569,10 @@ def main(argv=None):
             dist.init_process_group(backend)
     if dist_on and cfg["kind"] == "merge":
         from paper_1406_2628_b200.multigpu import bench_distributed
-        res = bench_distributed(args, cfg, ws, rank, local)
+        res = bench_distributed(args, cfg, ws, rank, local, lambda: ClockSampler(local))
     elif dist_on:
         from paper_1406_2628_b200.multigpu import bench_distributed_sort
-        res = bench_distributed_sort(args, cfg, ws, rank, local)
+        res = bench_distributed_sort(args, cfg, ws, rank, local, lambda: ClockSampler(local))
     else:
         res = run_ours(args, cfg, ws, rank, local, dist_on)
     if rank == 0:

@@ -61,6 +61,8 @@ typedef enum mp_status {
 const char *mp_last_error(void);
 /* ABI version (major*100 + minor). */
 int mp_abi_version(void);
+/* Kernels this library has launched in the process so far (all threads). */
+uint64_t mp_launch_count(void);
 /* Size in bytes of one key of `key_type` (0 if unknown). */
 uint64_t mp_key_size(int key_type);
 

@@ -25,6 +25,7 @@ _u64, _i, _p = C.c_uint64, C.c_int, C.c_void_p
 SIGNATURES = [
     ("mp_last_error", C.c_char_p, []),
     ("mp_abi_version", _i, []),
+    ("mp_launch_count", _u64, []),
     ("mp_key_size", _u64, [_i]),
     ("mp_partition", _i, [_i, _p, _u64, _p, _u64, _u64, _p, _p, _p]),
     ("mp_diagonal_search", _i, [_i, _p, _u64, _p, _u64, _p, _u64, _p, _p, _p]),

@@ -15,6 +15,7 @@
 
 #include "../../include/mergepath_b200.h"
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <vector>
 
@@ -51,8 +52,13 @@ int cuda_fail(cudaError_t e, const char *what) {
       return cuda_fail(e_, #x);                                                \
   } while (0)
 
+// Every kernel launch of the library is followed by MP_LAUNCHED, which also
+// counts it (mp_launch_count: the bench's gpu_launches is this counter).
+std::atomic<uint64_t> g_launches{0};
+
 #define MP_LAUNCHED(what)                                                      \
   do {                                                                         \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                        \
     const cudaError_t e_ = cudaGetLastError();                                 \
     if (e_ != cudaSuccess)                                                     \
       return cuda_fail(e_, what);                                              \
@@ -1082,6 +1088,7 @@ extern "C" {
 
 const char *mp_last_error(void) { return g_err.c_str(); }
 int mp_abi_version(void) { return 100; }
+uint64_t mp_launch_count(void) { return g_launches.load(); }
 uint64_t mp_key_size(int key_type) { return key_size(key_type); }
 
 int mp_partition(int kt, const void *a, uint64_t na, const void *b,

@@ -594,7 +594,18 @@ def sharded_sort(x_local: torch.Tensor, vals=None, key_type=None, group=None,
 # --------------------------------------------------------------------------
 # bench.py --gpus N (N > 1): weak scaling, one process per GPU over NCCL
 # --------------------------------------------------------------------------
-def bench_distributed(args, cfg, ws, rank, local):
+class _NoClock:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+    def summary(self):
+        return None
+
+
+def bench_distributed(args, cfg, ws, rank, local, clock=None):
     """Each rank holds a fixed-size shard (the config's |A| and |B| per GPU)
     of globally sorted A and B (generated with the SplitMix64 counter
     generator at the rank's global offsets, then sorted across the ranks
@@ -637,14 +648,17 @@ def bench_distributed(args, cfg, ws, rank, local):
     torch.cuda.synchronize()
     dist.barrier()
     times = []
-    for _ in range(args.steps):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        out, _ = step()
-        e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
+    c0 = N.lib.mp_launch_count()
+    with (clock or _NoClock)() as clk:
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out, _ = step()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = N.lib.mp_launch_count() - c0
     dist.barrier()
     ms = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -683,18 +697,18 @@ def bench_distributed(args, cfg, ws, rank, local):
                                   + ("NVLink pull fused into the merge kernels via CUDA IPC"
                                      if transport == "p2p" else "NCCL all_to_all exchange") + ")",
                    "l2": "inputs+output larger than L2 (no flush needed)"},
-        "gpu_launches": None,
+        "gpu_launches": launches,
         "roofline": {"bound": "hbm+nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
                      "note": "per-rank algorithmic HBM bytes / step time; the exchange also "
                              "moves up to 4 B per remote element over NVLink"},
-        "clocks": None,
+        "clocks": clk.summary(),
         "e2e": {"value": total * e2e_steps / float(el.item()), "unit": "elements/s",
                 "h2d_bytes_per_step": (na + nb) * ks, "d2h_bytes_per_step": (na + nb) * ks},
     }
 
 
-def bench_distributed_sort(args, cfg, ws, rank, local):
+def bench_distributed_sort(args, cfg, ws, rank, local, clock=None):
     """bench.py --config 4 --gpus N: strong scaling of the 2^30-key sort
     (BASELINE config 4: each GPU local-sorts a 1/P shard, then Merge Path
     rounds across GPUs).  Shard r = keys [r*n/P, (r+1)*n/P) of the seed-4
@@ -716,14 +730,17 @@ def bench_distributed_sort(args, cfg, ws, rank, local):
     torch.cuda.synchronize()
     dist.barrier()
     times = []
-    for _ in range(args.steps):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        sorter.run(x)
-        e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
+    c0 = N.lib.mp_launch_count()
+    with (clock or _NoClock)() as clk:
+        for _ in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sorter.run(x)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = N.lib.mp_launch_count() - c0
     red_dev = dev if dist.get_backend() == "nccl" else torch.device("cpu")
     ms = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -753,13 +770,13 @@ def bench_distributed_sort(args, cfg, ws, rank, local):
                    "parallelism": f"local sort + {(ws - 1).bit_length()} cross-GPU Merge Path "
                                   "rounds, NVLink pull fused into the merge (CUDA IPC)",
                    "l2": "inputs+output larger than L2 (no flush needed)"},
-        "gpu_launches": None,
+        "gpu_launches": launches,
         "roofline": {"bound": "hbm+nvlink", "unit": "GB/s",
                      "achieved": (n // ws) * 8 * passes / (ms / args.steps / 1e3) / 1e9,
                      "peak": 6554.2, "frac": (n // ws) * 8 * passes / (ms / args.steps / 1e3)
                      / 1e9 / 6554.2, "traffic": None,
                      "note": f"per-GPU {passes} passes x 8 B/key over the step time"},
-        "clocks": None,
+        "clocks": clk.summary(),
         "e2e": {"value": n * e2e_steps / float(el.item()), "unit": "keys/s",
                 "h2d_bytes_per_step": (hi - lo) * 4, "d2h_bytes_per_step": (hi - lo) * 4},
     }
