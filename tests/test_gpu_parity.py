@@ -552,3 +552,49 @@ def test_large_merge_unaligned_inputs(cuda, port):
         want, _, _, _ = port.merge("u32", a, b)
         got = mp.parallel_merge(da[oa:oa + 1_200_001], db[ob:ob + 1_100_000], 4)
         assert np.array_equal(got.cpu().numpy(), want), (oa, ob)
+
+
+def test_host_pipeline_many_chunks(cuda):
+    """mp_merge_host's chunked PCIe pipeline (1 MiB chunks, read once per
+    process, hence the subprocess): page-widened H2D copies at unaligned
+    host offsets, ragged and empty sides, with and without values, against a
+    stable numpy merge (ties to A)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1406_2628_b200 import _native as N
+rng = np.random.default_rng(9)
+bad = []
+for kt, dt in ((0, np.uint32), (1, np.int32), (3, np.uint64), (4, np.int64)):
+    for na, nb, dup, off in ((3_000_001, 2_500_003, 1 << 30, 1), (1_234_567, 0, 50, 3),
+                             (5, 4_000_000, 7, 2), (2_000_000, 2_000_000, 1 << 20, 0)):
+        ba = np.sort(rng.integers(0, dup, na + off).astype(dt))
+        bb = np.sort(rng.integers(0, dup, nb + off).astype(dt))
+        a, b = ba[off:], bb[off:]  # host pointers off the allocation start
+        av = np.arange(na, dtype=np.uint32)
+        bv = np.arange(nb, dtype=np.uint32) | np.uint32(1 << 31)
+        cat = np.concatenate([a, b])
+        perm = np.argsort(cat, kind="stable")
+        for vals in (False, True):
+            out = np.empty(na + nb, dtype=dt)
+            outv = np.empty(na + nb, dtype=np.uint32) if vals else None
+            p = lambda x: x.ctypes.data if x is not None else None
+            N.check(N.lib.mp_merge_host(kt, p(a), p(av) if vals else None, na, p(b),
+                                        p(bv) if vals else None, nb, p(out), p(outv), 0))
+            ok = np.array_equal(out, cat[perm])
+            if vals:
+                ok = ok and np.array_equal(outv, np.concatenate([av, bv])[perm])
+            if not ok:
+                bad.append((kt, na, nb, vals))
+print("BAD", bad)
+sys.exit(1 if bad else 0)
+'''
+    from pathlib import Path
+    env = dict(os.environ, MP_HOST_CHUNK_MB="1")
+    r = subprocess.run([sys.executable, "-c", code, str(Path(__file__).resolve().parents[1])],
+                       env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
