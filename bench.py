@@ -56,11 +56,22 @@ CONFIGS = {
     "3b": dict(kind="merge", key="u64", gen=(4, 3), na=1 << 29, nb=1 << 25, bytes_per=24, vals=True,
                desc="config3b: stable merge u64 key + u32 value, |A|=2^29 |B|=2^25, B below A"),
     "4": dict(kind="sort", key="u32", gen=(0, None), n=1 << 30, bytes_per=160,
-              desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 2048-key block sort + 19 rounds"),
+              desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 4352-key block sort + 18 rounds"),
     "5": dict(kind="merge", key="f32", gen=(5, 6), na=1 << 31, nb=1 << 31, bytes_per=8,
               desc="config5: stable merge f32 |A|=|B|=2^31, A~Normal(0,1), B~Exp(1), IEEE "
                    "totalOrder (one GPU: the whole merge; --gpus 8: sharded)"),
 }
+BARE_RUN = 4352  # mp_sort's block-sort run for bare 32-bit keys (256 threads x 17)
+
+
+def sort_rounds(n: int, run: int = BARE_RUN) -> int:
+    """Merge rounds of mp_sort after the block sort (runs double per round)."""
+    r, w = 0, run
+    while w < n:
+        w, r = 2 * w, r + 1
+    return r
+
+
 KT = {"u32": 0, "i32": 1, "f32": 2, "u64": 3, "i64": 4}
 KSIZE = {"u32": 4, "i32": 4, "f32": 4, "u64": 8, "i64": 8}
 
@@ -232,8 +243,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
                                          scratch.data_ptr(), scratch_b, stream.cuda_stream))
                 if evs is not None:
                     evs[1].record(stream)
-            rounds = max(0, (max(n, 1) - 1).bit_length() - 11)
-            launches_per_step = 1 + 2 * rounds
+            launches_per_step = 2 * sort_rounds(n) + (n >= BARE_RUN) + (n % BARE_RUN > 0)
             units = n
 
         for _ in range(args.warmup):
@@ -268,8 +278,8 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
         alg_bytes = n * cfg["bytes_per"]  # read A+B once, write S once
         kname = "merge_tiles_kernel (K2); step = K1 grid-snapped split search + K2"
     else:
-        alg_bytes = n * 8 * (1 + max(0, (n - 1).bit_length() - 11))
-        kname = "mp_sort: block_sort + 19 x (round_partition + merge_tiles)"
+        alg_bytes = n * 8 * (1 + sort_rounds(n))
+        kname = "mp_sort: block_sort_bare + 18 x (round_partition + merge_tiles)"
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
     tpath = ROOT / "profiles" / f"traffic_config{args.config}.json"

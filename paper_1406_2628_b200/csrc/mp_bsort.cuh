@@ -1,0 +1,190 @@
+// mp_bsort.cuh -- K3b: block sort for bare 32-bit keys (u32, i32, f32
+// totalOrder), the first pass of mp_sort when no values ride along
+// (replaces sort.hpp:59-67's insertion-sorted base runs).
+//
+// Bare keys carry no payload, so equal keys are indistinguishable: any
+// correct sort of a block yields the bytes of the stable one, and the keys
+// may be dealt to threads in any order.  The kernel is issue-bound, so the
+// design minimises instructions per key:
+//   * keys enter as their order-preserving u32 image (i32: sign flip, f32:
+//     totalOrder image) -- one unsigned compare per merge step for all three
+//     types -- and leave through the inverse image;
+//   * keys come in as 16-byte vectors (any dealing to threads is fine) and
+//     leave through one bulk store (cp.async.bulk) of the staged block;
+//   * a Batcher network sorts each thread's VT keys in registers;
+//   * log2(NT) Merge Path passes (core.hpp:99-180) in shared memory.  Each run
+//     of the pass is followed by one word holding the sentinel 0xFFFFFFFF,
+//     and A's cursor saturates at its sentinel, so the per-output step needs
+//     no bounds tests: once A is exhausted its sentinel loses to every B key
+//     below the maximum and ties with a B key equal to it -- which emits the
+//     same value, so the output bytes are exact.  (B's cursor cannot pass
+//     its sentinel: the sentinel is never strictly below an A key.)
+//     VT is odd, so the stride-VT stores hit 32 distinct banks and the
+//     merge cursors of neighbouring threads (~VT/2 apart) spread over banks.
+#pragma once
+
+#include "mp_common.cuh"
+
+namespace mpb {
+
+template <class KT> __device__ __forceinline__ uint32_t order_u32(typename KT::T x);
+template <> __device__ __forceinline__ uint32_t order_u32<KeyU32>(uint32_t x) { return x; }
+template <> __device__ __forceinline__ uint32_t order_u32<KeyI32>(int32_t x) {
+  return static_cast<uint32_t>(x) ^ 0x80000000u;
+}
+template <> __device__ __forceinline__ uint32_t order_u32<KeyF32>(uint32_t x) {
+  return f32_order(x);
+}
+template <class KT> __device__ __forceinline__ typename KT::T from_order_u32(uint32_t u);
+template <> __device__ __forceinline__ uint32_t from_order_u32<KeyU32>(uint32_t u) { return u; }
+template <> __device__ __forceinline__ int32_t from_order_u32<KeyI32>(uint32_t u) {
+  return static_cast<int32_t>(u ^ 0x80000000u);
+}
+template <> __device__ __forceinline__ uint32_t from_order_u32<KeyF32>(uint32_t u) {
+  return (u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u;  // inverse of f32_order
+}
+
+// smem: the finest level (NT runs of VT) has the most sentinel words
+template <int NT, int VT>
+__host__ __device__ constexpr uint32_t bare_sort_smem_bytes() {
+  return static_cast<uint32_t>(NT) * (VT + 1) * 4 + 64;
+}
+
+__device__ __forceinline__ void ce_u32(uint32_t &x, uint32_t &y) {
+  const uint32_t lo = min(x, y);
+  y = max(x, y);
+  x = lo;
+}
+
+// Batcher's odd-even merge sort network for the next power of two above N,
+// truncated to N inputs (the missing inputs act as +inf, so comparators that
+// touch them never fire and are dropped).
+template <int N>
+__device__ __forceinline__ void batcher_u32(uint32_t (&x)[N]) {
+  constexpr int P2 = N <= 1 ? 1 : 1 << (32 - __builtin_clz(N - 1));
+#pragma unroll
+  for (int p = 1; p < P2; p <<= 1) {
+#pragma unroll
+    for (int k = p; k >= 1; k >>= 1) {
+#pragma unroll
+      for (int j = k % p; j + k < P2; j += 2 * k) {
+#pragma unroll
+        for (int i = 0; i < k; ++i) {
+          if (i + j + k < N && (i + j) / (2 * p) == (i + j + k) / (2 * p))
+            ce_u32(x[i + j], x[i + j + k]);
+        }
+      }
+    }
+  }
+}
+
+// One CTA sorts NV = NT * VT keys (VT odd).  Pass k merges runs of
+// w = VT << k held by 2^k threads each; the pair of thread t is t >> (k+1).
+// Level-k layout: run r at word r * (w + 1), its sentinel at r * (w + 1) + w.
+template <class KT, int NT, int VT, bool ALIGNED>
+__global__ void __launch_bounds__(NT, 2048 / NT)
+    block_sort_bare_kernel(const typename KT::T *__restrict__ in,
+                           typename KT::T *__restrict__ out, uint64_t n,
+                           uint64_t block0) {
+  static_assert(sizeof(typename KT::T) == 4 && (VT & 1) && (NT & (NT - 1)) == 0,
+                "bare 32-bit keys, odd VT, NT a power of two");
+  constexpr int NV = NT * VT;
+  constexpr int LNT = __builtin_ctz(NT);
+  static_assert((NV * 4) % 16 == 0, "bulk store granularity");
+  extern __shared__ __align__(128) uint32_t s[];
+  const int tid = threadIdx.x;
+  const uint64_t base = (block0 + blockIdx.x) * NV;
+  // ALIGNED launches cover whole 16 B-aligned blocks only (the host sends a
+  // short last block or unaligned buffers to the generic instantiation)
+  const int cnt = ALIGNED ? NV : static_cast<int>((n - base) < NV ? (n - base) : NV);
+  constexpr bool full = ALIGNED;
+
+  // ---- load: any dealing of the block's keys to threads will do ----
+  uint32_t x[VT];
+  if constexpr (full) {
+    constexpr int V4 = NV / 4 / NT;  // 16-byte vectors per thread
+    const uint4 *src = reinterpret_cast<const uint4 *>(in + base);
+#pragma unroll
+    for (int m = 0; m < V4; ++m) {
+      const uint4 v = __ldg(src + tid + m * NT);
+      x[4 * m + 0] = order_u32<KT>(static_cast<typename KT::T>(v.x));
+      x[4 * m + 1] = order_u32<KT>(static_cast<typename KT::T>(v.y));
+      x[4 * m + 2] = order_u32<KT>(static_cast<typename KT::T>(v.z));
+      x[4 * m + 3] = order_u32<KT>(static_cast<typename KT::T>(v.w));
+    }
+#pragma unroll
+    for (int k = 4 * V4; k < VT; ++k)
+      x[k] = order_u32<KT>(in[base + (k - 4 * V4) * NT + 4 * V4 * NT + tid]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+      const int q = tid + k * NT;
+      x[k] = q < cnt ? order_u32<KT>(in[base + q]) : 0xFFFFFFFFu;
+    }
+  }
+  batcher_u32<VT>(x);
+
+#pragma unroll 1
+  for (int k = 0; k < LNT; ++k) {
+    const int w = VT << k;
+    // ---- store the thread's sorted VT keys (stride VT, odd: no conflicts) ----
+    {
+      const int r = tid >> k, off = (tid & ((1 << k) - 1)) * VT;
+      const int o = r * (w + 1) + off;
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        s[o + q] = x[q];
+      if (off + VT == w)
+        s[o + VT] = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    // ---- split: diagonal search within the pair (ties to A) ----
+    const int diag = (tid & ((2 << k) - 1)) * VT;
+    const int aO = ((tid >> (k + 1)) << 1) * (w + 1);
+    const int bO = aO + w + 1;
+    int lo = diag > w ? diag - w : 0;
+    int hi = diag < w ? diag : w;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s[bO + diag - 1 - mid] < s[aO + mid])
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    // ---- serial merge of VT outputs, no bounds tests (see header) ----
+    int pa = aO + lo, pb = bO + (diag - lo);
+    const int ea = aO + w;  // A's sentinel
+    uint32_t ka = s[pa], kb = s[pb];
+#pragma unroll
+    for (int q = 0; q < VT; ++q) {
+      const bool tb = kb < ka;
+      x[q] = tb ? kb : ka;
+      pa = tb ? pa : min(pa + 1, ea);
+      pb = tb ? pb + 1 : pb;
+      const uint32_t nx = s[tb ? pb : pa];
+      kb = tb ? nx : kb;
+      ka = tb ? ka : nx;
+    }
+    __syncthreads();
+  }
+
+  // ---- x = sorted positions [tid*VT, tid*VT + VT); stage, write back ----
+#pragma unroll
+  for (int q = 0; q < VT; ++q)
+    s[tid * VT + q] = static_cast<uint32_t>(from_order_u32<KT>(x[q]));
+  if constexpr (full) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(out + base, s, NV * 4);
+      bulk_commit();
+      bulk_wait_read0();
+    }
+  } else {
+    __syncthreads();
+    for (int q = tid; q < cnt; q += NT)
+      out[base + q] = static_cast<typename KT::T>(s[q]);
+  }
+}
+
+}  // namespace mpb

@@ -23,6 +23,7 @@
 #include "mp_spm.cuh"
 #include "mp_pieces.cuh"
 #include "mp_radix.cuh"
+#include "mp_bsort.cuh"
 
 namespace {
 
@@ -144,7 +145,10 @@ template <class KT> struct SortMergeCfg {
 constexpr int kBlockNT = 128;
 constexpr int kBlockVT = 16;
 constexpr uint64_t kRun = kBlockNT * kBlockVT;  // 2048-key block-sort runs
-static_assert(kRun == 2048, "round pshift assumes 2048-key runs");
+// bare 32-bit keys: K3b (mp_bsort.cuh), 4096-key runs
+constexpr int kBareNT = 256;
+constexpr int kBareVT = 17;  // odd: conflict-free strided smem stores
+constexpr uint64_t kBareRun = kBareNT * kBareVT;
 
 template <class K> cudaError_t set_smem(K kernel, uint32_t bytes) {
   if (bytes <= 48 * 1024)
@@ -470,8 +474,20 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   uint32_t *auxv = VALS ? reinterpret_cast<uint32_t *>(ws + L.vals_off) : nullptr;
   uint64_t *P = reinterpret_cast<uint64_t *>(ws + L.part_off);
 
+  // MP_BLOCK_SORT=radix: LSD radix block sort for bare 32-bit keys (same
+  // bytes).  Opt-in: measured on B200 at 30.0 ms for 2^30 keys vs 8.3 ms for
+  // the merge-based block sort (match.any ranking + 1.7 G bank conflicts),
+  // though it issues 35 % fewer instructions.  MP_BLOCK_SORT=merge: the
+  // general merge-based block sort K3 for bare keys too (A/B testing).
+  static const int bs_engine = [] {
+    const char *e = std::getenv("MP_BLOCK_SORT");
+    return !e ? 0 : std::strcmp(e, "radix") == 0 ? 1 : std::strcmp(e, "merge") == 0 ? 2 : 0;
+  }();
+  constexpr bool kBare4 = !VALS && sizeof(T) == 4 && KT::kind != kElement;
+  const bool use_bare = kBare4 && bs_engine == 0;
+  const uint64_t run0 = use_bare ? kBareRun : kRun;
   int rounds = 0;
-  for (uint64_t w = kRun; w < n; w *= 2)
+  for (uint64_t w = run0; w < n; w *= 2)
     ++rounds;
   // Block sort lands where an even/odd number of ping-pong rounds ends in
   // `keys` (the result always lands back in the caller's buffer).
@@ -481,17 +497,26 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   T *dst = in_place ? aux : keys;
   uint32_t *dstv = in_place ? auxv : vals;
 
-  // MP_BLOCK_SORT=radix: LSD radix block sort for bare 32-bit keys (same
-  // bytes).  Opt-in: measured on B200 at 30.0 ms for 2^30 keys vs 8.3 ms for
-  // the merge-based block sort (match.any ranking + 1.7 G bank conflicts),
-  // though it issues 35 % fewer instructions.
-  static const bool radix_bs = [] {
-    const char *e = std::getenv("MP_BLOCK_SORT");
-    return e && std::strcmp(e, "radix") == 0;
-  }();
   bool block_sorted = false;
-  if constexpr (!VALS && sizeof(T) == 4 && KT::kind != kElement) {
-    if (radix_bs) {
+  if constexpr (kBare4) {
+    if (use_bare) {
+      constexpr uint32_t smem = bare_sort_smem_bytes<kBareNT, kBareVT>();
+      const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+      const uint64_t whole = al ? n / kBareRun : 0, blocks = cdiv(n, kBareRun);
+      if (whole) {
+        auto kern = block_sort_bare_kernel<KT, kBareNT, kBareVT, true>;
+        MP_CUDA(set_smem(kern, smem));
+        kern<<<static_cast<unsigned>(whole), kBareNT, smem, s>>>(in, src, n, 0);
+        MP_LAUNCHED("block_sort_bare_kernel");
+      }
+      if (blocks > whole) {
+        auto kern = block_sort_bare_kernel<KT, kBareNT, kBareVT, false>;
+        MP_CUDA(set_smem(kern, smem));
+        kern<<<static_cast<unsigned>(blocks - whole), kBareNT, smem, s>>>(in, src, n, whole);
+        MP_LAUNCHED("block_sort_bare_kernel(tail)");
+      }
+      block_sorted = true;
+    } else if (bs_engine == 1) {
       static_assert(kRadixNV == kRun, "radix block = sort run");
       constexpr uint32_t smem = radix_smem_bytes();
       auto kern = block_radix_sort_kernel<KT>;
@@ -512,21 +537,25 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   }
 
   constexpr int NT = SortMergeCfg<KT>::NT, VT = SortMergeCfg<KT>::VT;
-  constexpr uint32_t NV = SortMergeCfg<KT>::TILE;
-  static_assert(NT * VT >= int(NV) && (2 * kRun) % NV == 0, "round tile shape");
+  // round tile: TILE, or the bare block's run (4352 = 17 * 256) so that the
+  // tile divides every pair width with a power-of-two ratio
+  static_assert(NT * VT >= int(SortMergeCfg<KT>::TILE) && (2 * kRun) % SortMergeCfg<KT>::TILE == 0 &&
+                    (!kBare4 || NT * VT >= int(kBareRun)),
+                "round tile shape");
+  const uint32_t NV = use_bare ? static_cast<uint32_t>(kBareRun) : SortMergeCfg<KT>::TILE;
   const uint64_t tiles = cdiv(n, NV);
   constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
   auto kern = merge_tiles_kernel<KT, VALS, NT, VT, RoundMap, false>;
   MP_CUDA(set_smem(kern, smem));
-  uint32_t pshift = 12;  // 2 * kRun == 1 << 12
-  for (uint64_t w = kRun; w < n; w *= 2, ++pshift) {
+  uint32_t tshift = static_cast<uint32_t>(__builtin_ctzll(2 * run0 / NV));  // 2w = NV << tshift
+  for (uint64_t w = run0; w < n; w *= 2, ++tshift) {
     // K4 || K2 within the round (the round's input is complete)
     auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
       if (hi <= lo)
         return MP_OK;
       round_partition_kernel<KT>
           <<<static_cast<unsigned>(cdiv(hi - lo, 128)), 128, 0, st>>>(
-              src, n, w, pshift, NV, hi, P, lo);
+              src, n, w, tshift, NV, hi, P, lo);
       MP_LAUNCHED("round_partition_kernel");
       return MP_OK;
     };
@@ -534,7 +563,7 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
       if (t1 <= t0)
         return MP_OK;
       kern<<<static_cast<unsigned>(t1 - t0), NT, smem, st>>>(
-          RoundMap{P, n, w, NV, pshift}, src, srcv, src, srcv, dst, dstv,
+          RoundMap{P, n, w, NV, tshift}, src, srcv, src, srcv, dst, dstv,
           nullptr, t0);
       MP_LAUNCHED("merge_tiles_kernel(round)");
       return MP_OK;

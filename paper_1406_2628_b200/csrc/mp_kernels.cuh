@@ -175,17 +175,25 @@ struct PlainMap {
 
 // One bottom-up round over runs of `width` (sort.hpp:71-101): pair k merges
 // A = src[2kw, 2kw+w) with B = src[2kw+w, 2kw+2w) (clipped to n); an
-// unpaired tail run has an empty B and is copied.  NV divides 2w, so a tile
-// never straddles two pairs.  P[t] = a_off (pair-local) at the tile start.
+// unpaired tail run has an empty B and is copied.  The tile NV divides the
+// pair width 2w = NV << tshift, so a tile never straddles two pairs and the
+// pair of tile t is t >> tshift (widths need not be powers of two: the bare
+// 32-bit block sort makes 4352-key runs).  P[t] = pair-local a_off at the
+// tile start.
+__device__ __forceinline__ uint64_t round_pair_start(uint64_t t, uint32_t nv,
+                                                     uint32_t tshift) {
+  return (t >> tshift) * (uint64_t(nv) << tshift);
+}
+
 struct RoundMap {
   const uint64_t *P;
   uint64_t n;
-  uint64_t width;  // a power of two: 2 * width == 1 << pshift
+  uint64_t width;
   uint32_t nv;
-  uint32_t pshift;
+  uint32_t tshift;
   __device__ __forceinline__ TileWin window(uint64_t t) const {
     const uint64_t d0 = t * nv;
-    const uint64_t s = (d0 >> pshift) << pshift;
+    const uint64_t s = round_pair_start(t, nv, tshift);
     const uint64_t la = (n - s) < width ? (n - s) : width;
     const uint64_t rest = n - s - la;
     const uint64_t lb = rest < width ? rest : width;
@@ -207,7 +215,7 @@ struct RoundMap {
 template <class KT>
 __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
                                        uint64_t n, uint64_t width,
-                                       uint32_t pshift, uint32_t nv,
+                                       uint32_t tshift, uint32_t nv,
                                        uint64_t tiles,
                                        uint64_t *__restrict__ P,
                                        uint64_t t0 = 0) {
@@ -215,7 +223,7 @@ __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
   if (t >= tiles)
     return;
   const uint64_t d0 = t * nv;
-  const uint64_t s = (d0 >> pshift) << pshift;
+  const uint64_t s = round_pair_start(t, nv, tshift);
   const uint64_t la = (n - s) < width ? (n - s) : width;
   const uint64_t rest = n - s - la;
   const uint64_t lb = rest < width ? rest : width;
