@@ -24,6 +24,7 @@
 #include "mp_pieces.cuh"
 #include "mp_radix.cuh"
 #include "mp_bsort.cuh"
+#include "mp_quad.cuh"
 
 namespace {
 
@@ -429,8 +430,14 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
 
 // ---- K3 + (K4 + K2) x rounds: bottom-up merge sort ---------------------------
 struct SortLayout {
-  uint64_t keys_off, vals_off, part_off, total;
+  uint64_t keys_off, vals_off, part_off, quad_off, total;
 };
+// grid spacing of the fused two-round pass (mp_quad.cuh): the bare block
+// sort's run, so G divides every pair width 2w
+#ifndef MP_QUAD_DIV
+#define MP_QUAD_DIV 1  // G = 4352 / DIV (2176 measured slower: 3.71 ms)
+#endif
+constexpr uint32_t kQuadG = static_cast<uint32_t>(kBareRun) / MP_QUAD_DIV;
 
 template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
   using T = typename KT::T;
@@ -440,7 +447,8 @@ template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
   L.keys_off = 0;
   L.vals_off = up(n * sizeof(T));
   L.part_off = L.vals_off + (vals ? up(n * 4) : 0);
-  L.total = L.part_off + up((cdiv(n, NV) + 1) * sizeof(uint64_t));
+  L.quad_off = L.part_off + up((cdiv(n, NV) + 1) * sizeof(uint64_t));
+  L.total = L.quad_off + (!vals && sizeof(T) == 4 ? up((cdiv(n, kQuadG) + 4) * sizeof(QuadPt)) : 0);
   return L;
 }
 
@@ -489,9 +497,21 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   int rounds = 0;
   for (uint64_t w = run0; w < n; w *= 2)
     ++rounds;
-  // Block sort lands where an even/odd number of ping-pong rounds ends in
+  // MP_SORT_QUAD=1: fuse round pairs into one HBM pass (mp_quad.cuh).
+  // Opt-in: bit-exact, but measured on B200 (2^30 u32) at 3.48 ms (K5q) +
+  // 0.18 ms (K4q) per fused pass vs 2 x (1.25 + 0.11) ms for two plain
+  // rounds -- segments hold 0..2G outputs, so a CTA sized for 2G is half
+  // idle and 5 CTAs/SM cannot hide the serial-merge and load latencies.
+  static const bool quad_env = [] {
+    const char *e = std::getenv("MP_SORT_QUAD");
+    return e && std::strcmp(e, "1") == 0;
+  }();
+  const bool use_quad = use_bare && quad_env;
+  const int quad_passes = use_quad ? rounds / 2 : 0;
+  const int passes = rounds - quad_passes;  // ping-pong swaps after the block sort
+  // Block sort lands where an even/odd number of ping-pong passes ends in
   // `keys` (the result always lands back in the caller's buffer).
-  const bool in_place = (rounds % 2) == 0;
+  const bool in_place = (passes % 2) == 0;
   T *src = in_place ? keys : aux;
   uint32_t *srcv = in_place ? vals : auxv;
   T *dst = in_place ? aux : keys;
@@ -548,7 +568,42 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   auto kern = merge_tiles_kernel<KT, VALS, NT, VT, RoundMap, false>;
   MP_CUDA(set_smem(kern, smem));
   uint32_t tshift = static_cast<uint32_t>(__builtin_ctzll(2 * run0 / NV));  // 2w = NV << tshift
+  int fused_left = quad_passes;
   for (uint64_t w = run0; w < n; w *= 2, ++tshift) {
+    if constexpr (kBare4) {
+      if (fused_left > 0) {
+        // rounds (w, 2w) in one pass: K4q crossings + K5q segment merges
+        --fused_left;
+        QuadPt *QP = reinterpret_cast<QuadPt *>(ws + L.quad_off);
+        const uint32_t G = static_cast<uint32_t>(kQuadG);
+        const uint32_t lshift = static_cast<uint32_t>(__builtin_ctzll(4 * w / G));
+        const uint64_t full = n / (4 * w);
+        uint64_t lines = full << lshift;
+        if (full * 4 * w < n) {  // short last group
+          const uint64_t S = full * 4 * w;
+          uint64_t l[4];
+          for (int r = 0; r < 4; ++r) {
+            const uint64_t st = S + r * w;
+            l[r] = st < n ? std::min<uint64_t>(w, n - st) : 0;
+          }
+          lines += cdiv(l[0] + l[1], G) + cdiv(l[2] + l[3], G);
+        }
+        quad_partition_kernel<KT, kQuadG><<<static_cast<unsigned>(cdiv(lines, 128)), 128, 0, s>>>(
+            src, n, w, lshift, lines, QP);
+        MP_LAUNCHED("quad_partition_kernel");
+        constexpr int QNT = 2 * NT / MP_QUAD_DIV, QVT = VT;
+        static_assert(QNT / 2 * QVT >= int(kQuadG), "inner merges fit half a CTA");
+        constexpr uint32_t qsmem = merge_smem_bytes<KT, false, QNT, QVT>();
+        auto qkern = quad_merge_kernel<KT, QNT, QVT, kQuadG>;
+        MP_CUDA(set_smem(qkern, qsmem));
+        qkern<<<static_cast<unsigned>(lines), QNT, qsmem, s>>>(src, dst, n, w, lshift, QP);
+        MP_LAUNCHED("quad_merge_kernel");
+        std::swap(src, dst);
+        w *= 2;  // the loop's own doubling completes the second round
+        ++tshift;
+        continue;
+      }
+    }
     // K4 || K2 within the round (the round's input is complete)
     auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
       if (hi <= lo)

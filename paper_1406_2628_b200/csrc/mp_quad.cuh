@@ -1,0 +1,332 @@
+// mp_quad.cuh -- two bottom-up merge rounds in one pass over HBM.
+//
+// Rounds r and r+1 of sort.hpp:71-128 merge, for every group of four runs
+// R0..R3 of width w (group start S = 4gw, runs clipped to n):
+//     X = merge(R0, R1), Y = merge(R2, R3)        (round r, ties to the left)
+//     out = merge(X, Y)                            (round r+1, ties to X)
+// with an unpaired tail run carried, exactly as two separate rounds would.
+// The fused pass produces the same bytes without materialising X and Y:
+//
+// K4q (quad_partition_kernel): the merge path of (X, Y) is cut where it
+//   crosses the grid lines x = kG and y = jG (G divides 2w).  A crossing at
+//   x = kG is the element v = X[kG] (a diagonal search on R0/R1 gives its
+//   split (a, kG - a)); the Y elements before it are those < v, i.e.
+//   (lower_bound(R2, v), lower_bound(R3, v)).  A crossing at y = jG is
+//   u = Y[jG] (diagonal search on R2/R3); the X elements before it are those
+//   <= u (ties go to X): (upper_bound(R0, u), upper_bound(R1, u)).  Each
+//   crossing is thus a 4-way split (i0, i1, i2, i3) of the group.  The
+//   crossing at x = kG is preceded by ceil(y/G) y-crossings and vice versa,
+//   which gives every crossing its slot in path order directly.
+// K5q (quad_merge_kernel): one CTA per segment between consecutive
+//   crossings.  No grid line lies strictly inside a segment, so it holds at
+//   most G elements of X and G of Y: <= 2G outputs.  The CTA bulk-copies its four run slices
+//   into smem, merges R0/R1 (threads of the first half) and R2/R3 (second
+//   half) into registers, writes X and Y back over the windows, merges X
+//   with Y (all threads) and bulk-stores the segment.
+// Both inner merges and the outer one use take_b (ties to the left
+// operand), so the result is the two-round result byte for byte.
+#pragma once
+
+#include "mp_kernels.cuh"
+
+namespace mpb {
+
+struct QuadPt {
+  unsigned long long i[4];  // consumed prefix of R0..R3 at the crossing
+};
+
+struct QuadGroup {
+  uint64_t S;     // first element of the group
+  uint64_t l[4];  // run lengths (0 past n)
+};
+
+__device__ __forceinline__ QuadGroup quad_group(uint64_t g, uint64_t n,
+                                                uint64_t w) {
+  QuadGroup q;
+  q.S = g * 4 * w;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint64_t s = q.S + r * w;
+    q.l[r] = s < n ? (n - s < w ? n - s : w) : 0;
+  }
+  return q;
+}
+
+// number of elements < v
+template <class KT>
+__device__ __forceinline__ uint64_t lower_bound_dev(const typename KT::T *a,
+                                                    uint64_t n,
+                                                    typename KT::T v) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (KT::less(a[mid], v))
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// number of elements <= v
+template <class KT>
+__device__ __forceinline__ uint64_t upper_bound_dev(const typename KT::T *a,
+                                                    uint64_t n,
+                                                    typename KT::T v) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (KT::less(v, a[mid]))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint64_t cdiv_dev(uint64_t a, uint64_t b) {
+  return (a + b - 1) / b;
+}
+
+// K4q: one thread per grid line of a group; 4w/G = 1 << lshift lines per
+// full group.  P[(g << lshift) + slot] = the crossing in path order.
+template <class KT, uint32_t G>
+__global__ void quad_partition_kernel(const typename KT::T *__restrict__ src,
+                                      uint64_t n, uint64_t w, uint32_t lshift,
+                                      uint64_t lines, QuadPt *__restrict__ P) {
+  using T = typename KT::T;
+  const uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (p >= lines)
+    return;
+  const uint64_t g = p >> lshift;
+  const uint64_t u = p & ((uint64_t(1) << lshift) - 1);
+  const QuadGroup q = quad_group(g, n, w);
+  const T *R0 = src + q.S, *R1 = R0 + w, *R2 = R1 + w, *R3 = R2 + w;
+  const uint64_t cx = cdiv_dev(q.l[0] + q.l[1], G);
+  const uint64_t cy = cdiv_dev(q.l[2] + q.l[3], G);
+  QuadPt pt;
+  uint64_t slot;
+  if (u < cx) {
+    const uint64_t d = u * G;
+    const uint64_t a = diag_search_grid<KT>(R0, q.l[0], R1, q.l[1], d);
+    const uint64_t b = d - a;
+    const bool from_b = b < q.l[1] && (a >= q.l[0] || take_b<KT>(R1[b], R0[a]));
+    const T v = from_b ? R1[b] : R0[a];
+    const uint64_t i2 = lower_bound_dev<KT>(R2, q.l[2], v);
+    const uint64_t i3 = lower_bound_dev<KT>(R3, q.l[3], v);
+    pt.i[0] = a;
+    pt.i[1] = b;
+    pt.i[2] = i2;
+    pt.i[3] = i3;
+    slot = u + cdiv_dev(i2 + i3, G);
+  } else if (u - cx < cy) {
+    const uint64_t j = u - cx, d = j * G;
+    const uint64_t c = diag_search_grid<KT>(R2, q.l[2], R3, q.l[3], d);
+    const uint64_t e = d - c;
+    const bool from_b = e < q.l[3] && (c >= q.l[2] || take_b<KT>(R3[e], R2[c]));
+    const T v = from_b ? R3[e] : R2[c];
+    const uint64_t i0 = upper_bound_dev<KT>(R0, q.l[0], v);
+    const uint64_t i1 = upper_bound_dev<KT>(R1, q.l[1], v);
+    pt.i[0] = i0;
+    pt.i[1] = i1;
+    pt.i[2] = c;
+    pt.i[3] = e;
+    slot = j + cdiv_dev(i0 + i1, G);
+  } else {
+    return;  // the short last group has fewer lines
+  }
+  ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(P + (g << lshift) + slot);
+  dst[0] = make_ulonglong2(pt.i[0], pt.i[1]);
+  dst[1] = make_ulonglong2(pt.i[2], pt.i[3]);
+}
+
+// K5q: one CTA per segment.  NT threads, VT outputs each in the outer merge;
+// each half of the CTA covers one inner merge (NT/2 * VT >= G).
+template <class KT, int NT, int VT, uint32_t G>
+__global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
+    quad_merge_kernel(const typename KT::T *__restrict__ src,
+                      typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
+                      uint32_t lshift, const QuadPt *__restrict__ P) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  constexpr int HALF = NT / 2;
+  extern __shared__ __align__(128) char smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  const int tid = threadIdx.x;
+
+  // ---- setup by warp 0 only: the segment's crossings, four run slices and
+  //      their smem windows go to a header; lane 0 issues the bulk copies and
+  //      lanes 8r..8r+7 load window r's unaligned head/tail (< 16 B each) ----
+  static_assert(KS <= 8 || KS == 16, "edge lanes per window");
+  struct Hdr {
+    uint32_t oW[4];
+    int cnt[4];
+    unsigned long long o0;
+  };
+  Hdr *hdr = reinterpret_cast<Hdr *>(smem + 16);
+  constexpr uint32_t kWin0 = 64;
+  if (tid < 32) {
+    const uint64_t b = blockIdx.x;
+    const uint64_t g = b >> lshift;
+    const uint64_t m = b & ((uint64_t(1) << lshift) - 1);
+    const QuadGroup q = quad_group(g, n, w);
+    // crossings in this group: 4w/G for a whole group, fewer for the last
+    const uint64_t pts = q.S + 4 * w <= n
+                             ? (uint64_t(1) << lshift)
+                             : cdiv_dev(q.l[0] + q.l[1], G) + cdiv_dev(q.l[2] + q.l[3], G);
+    const QuadPt p0 = P[(g << lshift) + m];
+    QuadPt p1;
+    if (m + 1 < pts) {
+      p1 = P[(g << lshift) + m + 1];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        p1.i[r] = q.l[r];
+    }
+    int cnt[4];
+    const char *gW[4];
+    uint32_t oW[4];
+    uint32_t at = kWin0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      cnt[r] = static_cast<int>(p1.i[r] - p0.i[r]);
+      gW[r] = reinterpret_cast<const char *>(src + q.S + r * w + p0.i[r]);
+      oW[r] = mirror_off(at, gW[r]);
+      at = oW[r] + cnt[r] * KS;
+    }
+    const int l = tid;
+    if (l == 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        hdr->oW[r] = oW[r];
+        hdr->cnt[r] = cnt[r];
+      }
+      hdr->o0 = q.S + p0.i[0] + p0.i[1] + p0.i[2] + p0.i[3];
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      uint32_t lo[4], ib[4], tx = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        ib[r] = interior_bytes(gW[r], cnt[r] * KS, &lo[r]);
+        tx += ib[r];
+      }
+      mbar_arrive_expect_tx(bar, tx);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (ib[r])
+          bulk_g2s(smem + oW[r] + lo[r], gW[r] + lo[r], ib[r], bar);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if ((l >> 3) == r)
+        stage_edges<KS>(smem, oW[r], gW[r], cnt[r] * KS, l & 7);
+  }
+  __syncthreads();
+  uint32_t oW[4];
+  int cnt[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    oW[r] = hdr->oW[r];
+    cnt[r] = hdr->cnt[r];
+  }
+  const uint64_t o0 = hdr->o0;
+  const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
+  mbar_wait(bar, 0);
+
+  // ---- phase 1: X = merge(R0, R1) by threads [0, HALF), Y = merge(R2, R3)
+  //      by threads [HALF, NT), VT outputs each into registers ----
+  T keys[VT];
+  uint32_t vals[VT];
+  const int side = tid >= HALF ? 1 : 0;
+  const int t1 = tid - side * HALF;
+  const uint32_t oA = side ? oW[2] : oW[0], oB = side ? oW[3] : oW[1];
+  const int na = side ? cnt[2] : cnt[0], nb = side ? cnt[3] : cnt[1];
+  const int d1 = t1 * VT;
+  if (d1 < na + nb) {
+    int lo = d1 > nb ? d1 - nb : 0;
+    int hi = d1 < na ? d1 : na;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (take_b<KT>(lds<T>(smem, oB + (d1 - 1 - mid) * KS), lds<T>(smem, oA + mid * KS)))
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    serial_merge<KT, VT, false>(smem, oA, na, oB, nb, 0, 0, lo, d1 - lo, keys, vals);
+  }
+  __syncthreads();  // every window consumed
+  // X at [oX, oX + nx), Y right behind it (reads past X's end land in Y or
+  // the slack and are never used)
+  constexpr uint32_t oX = 16;
+  const uint32_t oY = oX + nx * KS;
+  {
+    const uint32_t op = side ? oY : oX;
+    const int lim = side ? ny : nx;
+    if (d1 + VT <= lim) {
+#pragma unroll
+      for (int k = 0; k < VT; ++k)
+        *reinterpret_cast<T *>(smem + op + (d1 + k) * KS) = keys[k];
+    } else if (d1 < lim) {
+#pragma unroll
+      for (int k = 0; k < VT; ++k)
+        if (d1 + k < lim)
+          *reinterpret_cast<T *>(smem + op + (d1 + k) * KS) = keys[k];
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2: out = merge(X, Y), ties to X ----
+  const int d2 = tid * VT;
+  if (d2 < total) {
+    int lo = d2 > ny ? d2 - ny : 0;
+    int hi = d2 < nx ? d2 : nx;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (take_b<KT>(lds<T>(smem, oY + (d2 - 1 - mid) * KS), lds<T>(smem, oX + mid * KS)))
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    serial_merge<KT, VT, false>(smem, oX, nx, oY, ny, 0, 0, lo, d2 - lo, keys, vals);
+  }
+  __syncthreads();  // X and Y consumed; stage the segment
+
+  // staging congruent (mod 16) to the output address: the 16 B-aligned
+  // interior leaves with one bulk store, the < 16 B head and tail by LSU
+  T *out = dst + o0;
+  const uint32_t oS = mirror_off(16, out);
+  if (d2 + VT <= total) {
+#pragma unroll
+    for (int k = 0; k < VT; ++k)
+      *reinterpret_cast<T *>(smem + oS + (d2 + k) * KS) = keys[k];
+  } else if (d2 < total) {
+#pragma unroll
+    for (int k = 0; k < VT; ++k)
+      if (d2 + k < total)
+        *reinterpret_cast<T *>(smem + oS + (d2 + k) * KS) = keys[k];
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  uint32_t lo;
+  const uint32_t ib = interior_bytes(reinterpret_cast<const char *>(out),
+                                     static_cast<uint32_t>(total) * KS, &lo);
+  if (tid == 0 && ib) {
+    bulk_s2g(reinterpret_cast<char *>(out) + lo, smem + oS + lo, ib);
+    bulk_commit();
+  }
+  if (tid >= 32 && tid < 64) {  // head [0, lo) and tail [lo + ib, total*KS)
+    const uint32_t bytes = static_cast<uint32_t>(total) * KS;
+    const uint32_t hi = ib ? lo + ib : bytes;
+    const uint32_t hlo = ib ? lo : bytes;
+    const uint32_t nh = hlo / KS, nt = (bytes - hi) / KS;
+    const uint32_t l = tid - 32;
+    if (l < nh + nt) {
+      const uint32_t e = l < nh ? l : (hi / KS) + (l - nh);
+      out[e] = lds<T>(smem, oS + e * KS);
+    }
+  }
+  if (tid == 0 && ib)
+    bulk_wait_read0();
+}
+
+}  // namespace mpb

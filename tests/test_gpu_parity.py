@@ -598,3 +598,59 @@ sys.exit(1 if bad else 0)
                        env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+_FUSED_SORT_CHECK = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import torch
+from test_gpu_parity import _fused_round_cases
+_fused_round_cases(torch.device("cuda", 0), sys.argv[2])
+print("FUSED OK")
+'''
+
+
+@pytest.mark.parametrize("S", ("u32", "i32", "f32"))
+@pytest.mark.parametrize("quad", ["0", "1"])
+def test_fused_round_sorts_vs_oracle(cuda, S, quad):
+    """Bare 32-bit sorts: the 4352-key block sort, then plain rounds
+    (default) or fused two-round passes (MP_SORT_QUAD=1, mp_quad.cuh; the
+    switch is read once per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", _FUSED_SORT_CHECK, root, S], capture_output=True,
+                       text=True, timeout=900, env=dict(os.environ, MP_SORT_QUAD=quad))
+    assert r.returncode == 0 and "FUSED OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def _fused_round_cases(cuda, S):
+    """Sizes straddle group boundaries (4 runs of 4352, 8704, ...) so the
+    short last group has 1, 2 or 3 runs; inputs include heavy duplicates,
+    all-equal, descending and (f32) signed zeros / NaNs."""
+    from oracle import bindings
+    from paper_1406_2628_b200 import mergepath as mp
+    port = bindings.port()
+    rng = np.random.default_rng(29)
+    R = 4352
+    sizes = (4 * R - 1, 4 * R, 4 * R + 1, 5 * R + 7, 6 * R, 7 * R + 3, 16 * R + 1,
+             16 * R + 9 * R, 64 * R - 5, 200_003, 1_000_000)
+    for n in sizes:
+        for kind in ("dup3", "uniform", "equal", "desc"):
+            if kind == "dup3":
+                d = _rand_unsorted(S, rng, n, 3)
+            elif kind == "uniform":
+                d = _rand_unsorted(S, rng, n, 1 << 30)
+            elif kind == "equal":
+                d = _rand_unsorted(S, rng, n, 1)
+            else:
+                d = np.sort(_rand_unsorted(S, rng, n, 1 << 20))[::-1].copy()
+            if S == "f32" and kind == "uniform":
+                d.view(np.uint32)[::97] = 0x80000000  # -0.0
+                d.view(np.uint32)[1::89] = 0x7FC00001  # NaN payloads
+                d.view(np.uint32)[2::101] = 0xFFC00000
+            want, _, _ = port.merge_sort(S, d)
+            got = mp.parallel_merge_sort(to_dev(d, S, cuda), 4, key_type=key_type(S))
+            assert same(from_dev(got, S), want), (S, n, kind)

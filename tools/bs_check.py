@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1406_2628_b200 import _native as N
 dev = torch.device("cuda", 0); st = torch.cuda.current_stream().cuda_stream
-res = {"engine": os.environ.get("MP_BLOCK_SORT", "radix")}
+res = {"block_sort": os.environ.get("MP_BLOCK_SORT", "default"), "quad": os.environ.get("MP_SORT_QUAD", "0")}
 for kt, dt, kind in ((0, torch.uint32, 0), (1, torch.int32, 1), (2, torch.float32, 5)):
     n = 1 << 30 if kt == 0 else (1 << 26) + 12345
     x = torch.empty(n, dtype=dt, device=dev)
