@@ -54,7 +54,9 @@ typedef enum mp_status {
   MP_ERR_INVALID = 1,     /* std::invalid_argument in the reference */
   MP_ERR_CUDA = 2,        /* CUDA launch / runtime failure */
   MP_ERR_OOM = 3,         /* device or pinned allocation failed */
-  MP_ERR_UNSUPPORTED = 4  /* key type / value combination not supported */
+  MP_ERR_UNSUPPORTED = 4, /* key type / value combination not supported */
+  MP_ERR_IO = 5           /* file I/O failure or truncated key file
+                             (std::runtime_error in dataio.cpp) */
 } mp_status;
 
 /* Message for the last non-OK status on this thread ("" if none). */
@@ -201,6 +203,26 @@ int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr);
  * on copies of the same device-generated bytes. */
 int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,
                 void *out, void *stream);
+
+/* ---- key files (dataio.hpp:5-25, dataio.cpp:33-98) -------------------- */
+/* Binary: "MPKB0001", u64 LE count, count x i64 LE keys.  Text: one integer
+ * per line (blank lines skipped).  Readers detect the format from the magic.
+ * Unparsable text -> MP_ERR_INVALID (naming the line); open/read/write
+ * failure or a truncated binary file -> MP_ERR_IO. */
+int mp_keyfile_count(const char *path, uint64_t *count, int *is_binary);
+int mp_keyfile_read(const char *path, int64_t *keys, uint64_t capacity,
+                    uint64_t *count);
+int mp_keyfile_write(const char *path, const int64_t *keys, uint64_t count,
+                     int binary);
+/* File -> device memory (i64 keys, MP_KEY_I64): a binary file is streamed
+ * through two pinned 32 MiB buffers, pread of chunk k+1 overlapping the H2D
+ * copy of chunk k.  Synchronous w.r.t. `stream` on return. */
+int mp_keyfile_load(const char *path, void *dev_keys, uint64_t capacity,
+                    uint64_t *count, int device, void *stream);
+/* Device memory -> binary key file (D2H of chunk k+1 overlaps the write of
+ * chunk k). */
+int mp_keyfile_store(const char *path, const void *dev_keys, uint64_t count,
+                     int device, void *stream);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libmergepath_b200.so"
 
-MP_OK, MP_ERR_INVALID, MP_ERR_CUDA, MP_ERR_OOM, MP_ERR_UNSUPPORTED = range(5)
+MP_OK, MP_ERR_INVALID, MP_ERR_CUDA, MP_ERR_OOM, MP_ERR_UNSUPPORTED, MP_ERR_IO = range(6)
 
 KEY_U32, KEY_I32, KEY_F32, KEY_U64, KEY_I64, KEY_ELEMENT = range(6)
 KEY_NAMES = {KEY_U32: "u32", KEY_I32: "i32", KEY_F32: "f32", KEY_U64: "u64",
@@ -26,6 +26,11 @@ SIGNATURES = [
     ("mp_last_error", C.c_char_p, []),
     ("mp_abi_version", _i, []),
     ("mp_launch_count", _u64, []),
+    ("mp_keyfile_count", _i, [C.c_char_p, _p, _p]),
+    ("mp_keyfile_read", _i, [C.c_char_p, _p, _u64, _p]),
+    ("mp_keyfile_write", _i, [C.c_char_p, _p, _u64, _i]),
+    ("mp_keyfile_load", _i, [C.c_char_p, _p, _u64, _p, _i, _p]),
+    ("mp_keyfile_store", _i, [C.c_char_p, _p, _u64, _i, _p]),
     ("mp_key_size", _u64, [_i]),
     ("mp_partition", _i, [_i, _p, _u64, _p, _u64, _u64, _p, _p, _p]),
     ("mp_diagonal_search", _i, [_i, _p, _u64, _p, _u64, _p, _u64, _p, _p, _p]),
@@ -85,6 +90,8 @@ def check(status: int) -> None:
     msg = lib.mp_last_error().decode(errors="replace")
     if status == MP_ERR_INVALID:
         raise ValueError(msg)
+    if status == MP_ERR_IO:
+        raise OSError(msg)  # the reference's std::runtime_error (dataio.cpp)
     raise MergePathError(status, msg)
 
 

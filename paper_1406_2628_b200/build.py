@@ -47,14 +47,39 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
-        return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(LIB) + ".tmp", str(CSRC / "mp_capi.cu")]
+TOOL_SRC = PKG / "tools" / "mergebench_b200.cpp"
+TOOL = PKG / "bin" / "mergebench_b200"
+CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+
+
+def build_tool(verbose: bool = False) -> Path:
+    """mergebench_b200: the reference tool's CLI contract over the drop-in
+    headers and the C ABI (g++ -std=c++20, linked to the in-tree library)."""
+    TOOL.parent.mkdir(exist_ok=True)
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++20", "-O2", "-Wall", "-Wextra", "-pthread",
+           "-I", str(ROOT / "include"), "-I", str(CUDA_HOME / "include"),
+           "-o", str(TOOL) + ".tmp", str(TOOL_SRC),
+           "-L", str(PKG), "-lmergepath_b200", "-Wl,-rpath,$ORIGIN/..",
+           "-L", str(CUDA_HOME / "lib64"), "-lcudart_static", "-ldl", "-lrt"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=ROOT)
-    os.replace(str(LIB) + ".tmp", LIB)
+    os.replace(str(TOOL) + ".tmp", TOOL)
+    return TOOL
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if force or not up_to_date():
+        cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(LIB) + ".tmp", str(CSRC / "mp_capi.cu")]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True, cwd=ROOT)
+        os.replace(str(LIB) + ".tmp", LIB)
+    if force or not TOOL.exists() or TOOL.stat().st_mtime < max(
+            LIB.stat().st_mtime, TOOL_SRC.stat().st_mtime,
+            *(p.stat().st_mtime for p in (ROOT / "include").rglob("*.h*"))):
+        build_tool(verbose)
     return LIB
 
 

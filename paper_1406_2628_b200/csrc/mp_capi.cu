@@ -1629,3 +1629,6 @@ int mp_sort_host(int kt, const void *keys, const uint32_t *vals, uint64_t n,
 }
 
 }  // extern "C"
+
+// key files (dataio.cpp:33-98) -> host / HBM
+#include "mp_keyfile.cuh"
