@@ -10,7 +10,12 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libmergepath_b200.so"
+import os as _os
+
+# MP_NATIVE_LIB: load a differently-compiled build of the same library
+# (tuning A/B runs, tools/variant_bench.sh); the product default is in-tree.
+LIB_PATH = Path(_os.environ.get("MP_NATIVE_LIB") or
+                Path(__file__).resolve().parent / "libmergepath_b200.so")
 
 MP_OK, MP_ERR_INVALID, MP_ERR_CUDA, MP_ERR_OOM, MP_ERR_UNSUPPORTED, MP_ERR_IO = range(6)
 

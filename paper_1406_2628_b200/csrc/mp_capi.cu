@@ -121,11 +121,25 @@ template <class KT> bool aligned_keys(const void *p) {
 #ifndef MP_MERGE_VT8
 #define MP_MERGE_VT8 11
 #endif
+// Bare 4-byte integer keys take twice the tile (NT 512): half the K1 split
+// searches, same K2 rate.  B200 A/B (200 steps, tools/variants): config 2
+// step 0.671 -> 0.662 ms; but u32 + values 0.662 -> 0.741 ms, config 3a
+// (u64 + values) 2.05 -> 2.43 ms and config 5 (f32) 6.37 -> 6.48 ms at 512,
+// so values, the checksum sink and other key types keep NT 256.
+#ifndef MP_MERGE_NT_I4
+#define MP_MERGE_NT_I4 512
+#endif
 template <class KT> struct MergeCfg {
-  static constexpr int NT = MP_MERGE_NT;
+  // the tile the split search (K1, mp_merge_plan) is planned at
+  static constexpr int NT =
+      (KT::kind == kU32 || KT::kind == kI32) ? MP_MERGE_NT_I4 : MP_MERGE_NT;
   static constexpr int VT = sizeof(typename KT::T) == 4   ? MP_MERGE_VT4
                             : sizeof(typename KT::T) == 8 ? MP_MERGE_VT8
                                                           : 7;
+  // the tile K2 runs at for a given payload: values / the register sink
+  // use NT 256; a plan at a wider tile is refined (refine_partition_kernel)
+  template <bool VALS, bool SINK>
+  static constexpr int exec_nt() { return (VALS || SINK) ? MP_MERGE_NT : NT; }
 };
 // Sort rounds: the tile (TILE outputs) must divide 2 * 2048 (block-sort run
 // length) so no tile straddles two run pairs.  TILE is a power of two, but
@@ -182,8 +196,13 @@ template <class KT> uint64_t merge_tiles(uint64_t n) {
   constexpr uint64_t NV = MergeCfg<KT>::NT * MergeCfg<KT>::VT;
   return cdiv(n, NV);
 }
+// + the refined (NT 256) split points when the plan tile is wider
 template <class KT> uint64_t merge_ws_bytes(uint64_t n) {
-  return n ? (merge_tiles<KT>(n) + 1) * sizeof(uint64_t) : 0;
+  if (!n)
+    return 0;
+  constexpr uint64_t NVe = uint64_t(MP_MERGE_NT) * MergeCfg<KT>::VT;
+  const uint64_t fine = MergeCfg<KT>::NT == MP_MERGE_NT ? 0 : cdiv(n, NVe) + 1;
+  return (merge_tiles<KT>(n) + 1 + fine) * sizeof(uint64_t);
 }
 
 // K1 at tile spacing: P[t] = a_off on diagonal t*NV.
@@ -207,12 +226,26 @@ int merge_exec(const void *a, const uint32_t *av, uint64_t na, const void *b,
                const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
                unsigned long long *sum, const uint64_t *P, cudaStream_t s) {
   using T = typename KT::T;
-  constexpr int NT = MergeCfg<KT>::NT, VT = MergeCfg<KT>::VT;
+  constexpr int NT = MergeCfg<KT>::template exec_nt<VALS, SINK>(), VT = MergeCfg<KT>::VT;
   constexpr uint32_t NV = NT * VT;
   const uint64_t n = na + nb;
   if (n == 0)
     return MP_OK;
-  const uint64_t tiles = merge_tiles<KT>(n);
+  const uint64_t tiles = cdiv(n, NV);
+  if constexpr (NT != MergeCfg<KT>::NT) {
+    // the plan is at the wider tile: refine it to this tile's split points
+    // (bounded searches between neighbouring planned points), stored behind
+    // the planned ones in the workspace
+    constexpr uint32_t R = MergeCfg<KT>::NT / NT;
+    static_assert(MergeCfg<KT>::NT % NT == 0, "plan tile = R exec tiles");
+    uint64_t *Pf = const_cast<uint64_t *>(P) + merge_tiles<KT>(n) + 1;
+    refine_partition_kernel<KT>
+        <<<static_cast<unsigned>(cdiv(tiles + 1, 128)), 128, 0, s>>>(
+            static_cast<const T *>(a), na, static_cast<const T *>(b), nb, P, NV, R,
+            tiles + 1, Pf);
+    MP_LAUNCHED("refine_partition_kernel");
+    P = Pf;
+  }
   constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
   auto kern = merge_tiles_kernel<KT, VALS, NT, VT, PlainMap, SINK>;
   MP_CUDA(set_smem(kern, smem));
@@ -388,14 +421,15 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
                const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
                unsigned long long *sum, cudaStream_t s) {
   using T = typename KT::T;
-  constexpr int NT = MergeCfg<KT>::NT, VT = MergeCfg<KT>::VT;
+  // one-shot: plan and merge at the payload's own tile
+  constexpr int NT = MergeCfg<KT>::template exec_nt<VALS, SINK>(), VT = MergeCfg<KT>::VT;
   constexpr uint32_t NV = NT * VT;
   const uint64_t n = na + nb;
   if (n == 0)
     return MP_OK;
   if (!VALS && !SINK && use_spm(n, out))
     return spm_merge<KT>(a, na, b, nb, out, s);
-  const uint64_t tiles = merge_tiles<KT>(n);
+  const uint64_t tiles = cdiv(n, NV);
   if (tiles >= (1ull << 31))
     return fail(MP_ERR_INVALID, "merge too large (%llu elements)",
                 (unsigned long long)n);

@@ -123,6 +123,40 @@ __global__ void partition_kernel(const typename KT::T *__restrict__ a,
   }
 }
 
+// Refine a split plan made at tile NV*R to tile NV: boundary f lies between
+// the planned points of its wider tile, so the search is bounded by them.
+template <class KT>
+__global__ void refine_partition_kernel(const typename KT::T *__restrict__ a,
+                                        uint64_t na,
+                                        const typename KT::T *__restrict__ b,
+                                        uint64_t nb,
+                                        const uint64_t *__restrict__ Pc,
+                                        uint32_t nv, uint32_t R, uint64_t count,
+                                        uint64_t *__restrict__ Pf) {
+  const uint64_t f = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (f >= count)
+    return;
+  const uint64_t c = f / R, r = f % R;
+  if (r == 0) {
+    Pf[f] = Pc[c];
+    return;
+  }
+  const uint64_t n = na + nb;
+  const uint64_t d = f * nv < n ? f * nv : n;
+  uint64_t lo = d > nb ? d - nb : 0;
+  uint64_t hi = d < na ? d : na;
+  lo = lo > Pc[c] ? lo : Pc[c];
+  hi = hi < Pc[c + 1] ? hi : Pc[c + 1];
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (take_b<KT>(b[d - 1 - mid], a[mid]))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  Pf[f] = lo;
+}
+
 // Arbitrary diagonals (used by the drop-in API for single searches and for
 // the segmented-merge plan).
 template <class KT>
