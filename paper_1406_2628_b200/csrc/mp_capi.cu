@@ -416,7 +416,7 @@ inline bool use_spm(uint64_t n, const void *out) {
          (reinterpret_cast<uintptr_t>(out) & 15) == 0;
 }
 
-template <class KT, bool VALS, bool SINK>
+template <class KT, bool VALS, bool SINK, bool PEER = false>
 int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
                const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
                unsigned long long *sum, cudaStream_t s) {
@@ -427,7 +427,7 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
   const uint64_t n = na + nb;
   if (n == 0)
     return MP_OK;
-  if (!VALS && !SINK && use_spm(n, out))
+  if (!VALS && !SINK && !PEER && use_spm(n, out))
     return spm_merge<KT>(a, na, b, nb, out, s);
   const uint64_t tiles = cdiv(n, NV);
   if (tiles >= (1ull << 31))
@@ -438,7 +438,7 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
     return rc;
   uint64_t *Pp = static_cast<uint64_t *>(P.p);
   constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
-  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, PlainMap, SINK>;
+  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, PlainMap, SINK, PEER>;
   MP_CUDA(set_smem(kern, smem));
   auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
     if (hi <= lo)
@@ -868,6 +868,25 @@ template <class KT> struct SegmentOp {
 // Merge of piece-concatenated sequences (mp_pieces.cuh): probe the piece
 // crossings on the device, cut the output range there, and run the plain
 // K1 + K2 merge on every segment straight from the (peer) piece pointers.
+// Is p memory of another device than `dev` (a peer mapping)?
+bool is_peer(const void *p, int dev) {
+  cudaPointerAttributes at{};
+  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice && at.device != dev;
+}
+// MP_PEER_LSU=1: use the LSU loader for every piece merge (tests the peer
+// path on a one-GPU box)
+bool peer_lsu_forced() {
+  static const bool f = [] {
+    const char *e = std::getenv("MP_PEER_LSU");
+    return e && std::strcmp(e, "1") == 0;
+  }();
+  return f;
+}
+
 template <class KT> struct PiecesOp {
   static int run(const mp_piece *pa, int npa, const mp_piece *pb, int npb,
                  uint64_t o0, uint64_t o1, void *out_, uint32_t *outv,
@@ -931,6 +950,8 @@ template <class KT> struct PiecesOp {
         ++k;
       return k;
     };
+    int dev = 0;
+    MP_CUDA(cudaGetDevice(&dev));
     T *out = static_cast<T *>(out_);
     for (size_t q = 0; q + 1 < pts.size(); ++q) {
       const uint64_t a0 = pts[q].first, b0 = pts[q].second;
@@ -941,12 +962,25 @@ template <class KT> struct PiecesOp {
       const T *ap = static_cast<const T *>(A.ptr[ka]) + (a0 - A.start[ka]);
       const T *bp = static_cast<const T *>(B.ptr[kb]) + (b0 - B.start[kb]);
       const uint64_t ob = a0 + b0 - o0;
+      // windows in another GPU's memory are read by LSU vector loads over
+      // NVLink (the bulk-copy engine is used for local memory only)
+      const bool peer = peer_lsu_forced() ||
+                        (a1 > a0 && is_peer(pa[ka].keys, dev)) ||
+                        (b1 > b0 && is_peer(pb[kb].keys, dev)) ||
+                        (vals && a1 > a0 && is_peer(pa[ka].vals, dev)) ||
+                        (vals && b1 > b0 && is_peer(pb[kb].vals, dev));
       int rc;
-      if (vals)
-        rc = merge_impl<KT, true, false>(
-            ap, pa[ka].vals + (a0 - A.start[ka]), a1 - a0, bp,
-            pb[kb].vals + (b0 - B.start[kb]), b1 - b0, out + ob, outv + ob,
-            nullptr, s);
+      const uint32_t *av_ = vals ? pa[ka].vals + (a0 - A.start[ka]) : nullptr;
+      const uint32_t *bv_ = vals ? pb[kb].vals + (b0 - B.start[kb]) : nullptr;
+      if (vals && peer)
+        rc = merge_impl<KT, true, false, true>(ap, av_, a1 - a0, bp, bv_, b1 - b0,
+                                               out + ob, outv + ob, nullptr, s);
+      else if (vals)
+        rc = merge_impl<KT, true, false>(ap, av_, a1 - a0, bp, bv_, b1 - b0,
+                                         out + ob, outv + ob, nullptr, s);
+      else if (peer)
+        rc = merge_impl<KT, false, false, true>(ap, nullptr, a1 - a0, bp, nullptr,
+                                                b1 - b0, out + ob, nullptr, nullptr, s);
       else
         rc = merge_impl<KT, false, false>(ap, nullptr, a1 - a0, bp, nullptr,
                                           b1 - b0, out + ob, nullptr, nullptr,

@@ -443,7 +443,21 @@ constexpr int block_sort_min_blocks() {
                                        : 1024 / NT;
 }
 
-template <class KT, bool VALS, int NT, int VT, class Map, bool SINK = false>
+// Interior copy by the LSU: 16-byte vector loads, all threads (the peer-
+// memory loader: NVLink reads of mapped peer pointers are plain LDG.128).
+template <int NT>
+__device__ __forceinline__ void lsu_copy16(char *smem, const char *g, uint32_t bytes,
+                                           int tid) {
+  const uint4 *src = reinterpret_cast<const uint4 *>(g);
+  uint4 *dst = reinterpret_cast<uint4 *>(smem);
+  for (uint32_t q = tid; q < bytes / 16; q += NT)
+    dst[q] = src[q];
+}
+
+// PEER = true: the window interiors arrive through LSU vector loads instead
+// of the bulk-copy engine (used for windows in another GPU's memory).
+template <class KT, bool VALS, int NT, int VT, class Map, bool SINK = false,
+          bool PEER = false>
 __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
     merge_tiles_kernel(Map map, const typename KT::T *__restrict__ a,
                        const uint32_t *__restrict__ av,
@@ -478,7 +492,19 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
     oBv = mirror_off(oAv + na_t * 4, gBv);
   }
 
-  if (tid == 0) {
+  if constexpr (PEER) {
+    uint32_t lo;
+    uint32_t in = interior_bytes(gA, bA, &lo);
+    lsu_copy16<NT>(smem + oA + lo, gA + lo, in, tid);
+    in = interior_bytes(gB, bB, &lo);
+    lsu_copy16<NT>(smem + oB + lo, gB + lo, in, tid);
+    if constexpr (VALS) {
+      in = interior_bytes(gAv, na_t * 4, &lo);
+      lsu_copy16<NT>(smem + oAv + lo, gAv + lo, in, tid);
+      in = interior_bytes(gBv, nb_t * 4, &lo);
+      lsu_copy16<NT>(smem + oBv + lo, gBv + lo, in, tid);
+    }
+  } else if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
     uint32_t loA, loB, loAv = 0, loBv = 0;
@@ -517,7 +543,8 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
     }
   }
   __syncthreads();
-  mbar_wait(bar, 0);
+  if constexpr (!PEER)
+    mbar_wait(bar, 0);
 
   // --- split the window among threads: diagonal search in smem ---
   const int diag = min(tid * VT, total);

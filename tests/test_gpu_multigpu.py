@@ -221,3 +221,16 @@ def test_p2p_sorter_processes(cuda, sizes):
     x = rng.integers(0, 1 << 20, sum(sizes)).astype(np.uint32)
     got = np.frombuffer(b"".join(res[r] for r in range(world)), dtype=np.uint32)
     assert np.array_equal(got, np.sort(x))
+
+
+def test_peer_lsu_loader_subprocess(cuda):
+    """The peer-memory loader of K2 (LSU vector loads instead of bulk
+    copies; chosen for windows on another GPU) forced on for every piece
+    merge (MP_PEER_LSU=1, read once per process) on the in-process piece
+    tests and the two-process P2P merger."""
+    import subprocess
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", str(Path(__file__)),
+                        "-k", "pieces or p2p_merger"], capture_output=True, text=True,
+                       timeout=900, env=dict(os.environ, MP_PEER_LSU="1"), cwd=str(ROOT))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
