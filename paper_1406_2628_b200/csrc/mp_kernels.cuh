@@ -431,7 +431,7 @@ template <class KT, bool VALS, int NT, bool SINK = false>
 constexpr int merge_min_blocks() {
   return (VALS && sizeof(typename KT::T) == 4)      ? 1024 / NT
          : (VALS || SINK)                           ? 1280 / NT
-         : sizeof(typename KT::T) == 4 && KT::kind != kF32 ? 2048 / NT
+         : sizeof(typename KT::T) == 4               ? 2048 / NT  // f32 too: B200 config 5 K2 5.77 -> 5.38 ms
          : sizeof(typename KT::T) <= 8               ? 1536 / NT
                                                      : 1280 / NT;
 }
