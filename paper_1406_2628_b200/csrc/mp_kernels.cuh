@@ -92,6 +92,9 @@ __device__ __forceinline__ uint64_t diag_search_grid(
   return lo;
 }
 
+#ifndef MP_K1_GRID
+#define MP_K1_GRID 16384  // B200 config 2 K1: 1024 34.0 us, 4096 27.2,
+#endif                    // 16384 24.8, 65536 23.7 (step 0.662 -> 0.650 ms)
 // Point t sits on diagonal min(t*spacing, N) (tile mode, p == 0) or on
 // floor(t*N/p) (p-way mode, core.hpp:90-92).  Writes a_off for t < count.
 template <class KT>
@@ -119,7 +122,7 @@ __global__ void partition_kernel(const typename KT::T *__restrict__ a,
     if (c)  // comparison count of the reference's search (core.hpp:128)
       atomicAdd(cmp, static_cast<unsigned long long>(c));
   } else {
-    a_offs[t] = diag_search_grid<KT>(a, na, b, nb, d);
+    a_offs[t] = diag_search_grid<KT, MP_K1_GRID>(a, na, b, nb, d);
   }
 }
 
@@ -261,7 +264,13 @@ __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
   const uint64_t la = (n - s) < width ? (n - s) : width;
   const uint64_t rest = n - s - la;
   const uint64_t lb = rest < width ? rest : width;
-  P[t] = diag_search_grid<KT>(src + s, la, src + s + la, lb, d0 - s);
+#ifndef MP_K4_GRID
+#define MP_K4_GRID 4096  // B200, 2^30 u32 sort, 18 rounds of K4: 0 (plain
+#endif                   // search) 2.70 ms, 256 2.94, 1024 2.08, 4096 1.76, 16384 1.83
+  if constexpr (MP_K4_GRID == 0)
+    P[t] = diag_search_global<KT>(src + s, la, src + s + la, lb, d0 - s);
+  else
+    P[t] = diag_search_grid<KT, MP_K4_GRID>(src + s, la, src + s + la, lb, d0 - s);
 }
 
 // ---------------------------------------------------------------------------
