@@ -654,3 +654,60 @@ def _fused_round_cases(cuda, S):
             want, _, _ = port.merge_sort(S, d)
             got = mp.parallel_merge_sort(to_dev(d, S, cuda), 4, key_type=key_type(S))
             assert same(from_dev(got, S), want), (S, n, kind)
+
+
+def test_beyond_2_32_elements(cuda):
+    """64-bit indexing end to end: a sort of 2^32 + 1001 u32 keys and a
+    merge with |A| + |B| > 2^32, verified on the device in 2^28-element
+    chunks (sortedness across chunk seams, per-chunk multiset fingerprint of
+    the low 16 bits and the key sum)."""
+    torch = _torch()
+    from paper_1406_2628_b200 import _native as N
+    free, _ = torch.cuda.mem_get_info()
+    if free < (80 << 30):
+        pytest.skip("needs ~60 GiB of device memory")
+    st = torch.cuda.current_stream().cuda_stream
+    C = 1 << 28
+
+    def fingerprint(x):
+        h = torch.zeros(65536, dtype=torch.int64, device=cuda)
+        s = 0
+        for i in range(0, x.numel(), C):
+            v = x[i:i + C].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+            h += torch.bincount(v & 0xFFFF, minlength=65536)
+            s += int(v.sum())
+        return h, s
+
+    def sorted_u32(x):
+        prev = None
+        for i in range(0, x.numel(), C):
+            v = x[i:i + C].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+            if not bool((v[1:] >= v[:-1]).all()) or (prev is not None and int(v[0]) < prev):
+                return False
+            prev = int(v[-1])
+        return True
+
+    n = (1 << 32) + 1001
+    x = torch.empty(n, dtype=torch.uint32, device=cuda)
+    N.check(N.lib.mp_generate(0, 9, 0, n, x.data_ptr(), st))
+    h0, s0 = fingerprint(x)
+    N.check(N.lib.mp_sort(N.KEY_U32, x.data_ptr(), None, n, None, 0, st))
+    torch.cuda.synchronize()
+    assert sorted_u32(x)
+    h1, s1 = fingerprint(x)
+    assert s1 == s0 and torch.equal(h1, h0)
+    na, nb = (1 << 31) + 3, (1 << 31) + 7
+    a = x[:na].clone()
+    del x
+    b = torch.empty(nb, dtype=torch.uint32, device=cuda)
+    N.check(N.lib.mp_generate(0, 2, 0, nb, b.data_ptr(), st))
+    N.check(N.lib.mp_sort(N.KEY_U32, b.data_ptr(), None, nb, None, 0, st))
+    out = torch.empty(na + nb, dtype=torch.uint32, device=cuda)
+    N.check(N.lib.mp_merge(N.KEY_U32, a.data_ptr(), None, na, b.data_ptr(), None, nb,
+                           out.data_ptr(), None, st))
+    torch.cuda.synchronize()
+    assert out.numel() > (1 << 32) and sorted_u32(out)
+    ha, sa = fingerprint(a)
+    hb, sb = fingerprint(b)
+    ho, so = fingerprint(out)
+    assert so == sa + sb and torch.equal(ho, ha + hb)
