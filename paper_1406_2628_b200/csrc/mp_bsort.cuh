@@ -188,3 +188,160 @@ __global__ void __launch_bounds__(NT, 2048 / NT)
 }
 
 }  // namespace mpb
+
+namespace mpb {
+
+// ---------------------------------------------------------------------------
+// K3w: block sort of 4096 bare 32-bit keys per CTA (256 threads x 16) that
+// keeps the first five merge levels in registers:
+//   * Batcher network on each thread's 16 keys (u32 order image);
+//   * warp levels m = 1..5 (groups of 2^m lanes, runs of 16 * 2^(m-1)
+//     merged): a bitonic merge of the two halves' ascending runs -- the
+//     "flip" stage compares element e with element 16*2^m - 1 - e (partner
+//     lane ^ (2^m - 1), register 15 - q), then half-cleaners at lane strides
+//     2^(m-2) .. 1 (shfl.xor) and register strides 8 .. 1 -- so a warp ends
+//     with one sorted run of 512 in lane-major order and no smem traffic;
+//   * three Merge Path passes in smem (runs of 512 -> 4096) with one
+//     sentinel word after every run and a p + p/32 padded layout (the
+//     stride-16 stores and loads stay conflict-free), A's cursor saturating
+//     at its sentinel as in K3b;
+//   * each thread's 16 sorted keys leave with four 16-byte stores.
+// Bare keys only (no stability question: equal keys are equal bytes).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ce_dir(uint32_t &x, uint32_t y, bool upper) {
+  x = upper ? max(x, y) : min(x, y);
+}
+
+__host__ __device__ __forceinline__ constexpr int pad32(int p) { return p + (p >> 5); }
+
+template <int NT>
+__host__ __device__ constexpr uint32_t warp_sort_smem_bytes() {
+  return static_cast<uint32_t>(pad32(NT * 16 + NT * 16 / 512 + 32)) * 4 + 64;
+}
+
+template <class KT, int NT, bool ALIGNED>
+__global__ void __launch_bounds__(NT, 2048 / NT)
+    block_sort_warp_kernel(const typename KT::T *__restrict__ in,
+                           typename KT::T *__restrict__ out, uint64_t n,
+                           uint64_t block0) {
+  static_assert(sizeof(typename KT::T) == 4 && NT % 32 == 0 && (NT & (NT - 1)) == 0,
+                "bare 32-bit keys, NT a power of two");
+  constexpr int VT = 16;
+  constexpr int NV = NT * VT;
+  extern __shared__ __align__(128) uint32_t s[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t base = (block0 + blockIdx.x) * NV;
+  const int cnt = ALIGNED ? NV : static_cast<int>((n - base) < NV ? (n - base) : NV);
+
+  uint32_t x[VT];
+  if constexpr (ALIGNED) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(in + base);
+#pragma unroll
+    for (int m = 0; m < VT / 4; ++m) {
+      const uint4 v = __ldg(src + tid + m * NT);
+      x[4 * m + 0] = order_u32<KT>(static_cast<typename KT::T>(v.x));
+      x[4 * m + 1] = order_u32<KT>(static_cast<typename KT::T>(v.y));
+      x[4 * m + 2] = order_u32<KT>(static_cast<typename KT::T>(v.z));
+      x[4 * m + 3] = order_u32<KT>(static_cast<typename KT::T>(v.w));
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+      const int q = tid + k * NT;
+      x[k] = q < cnt ? order_u32<KT>(in[base + q]) : 0xFFFFFFFFu;
+    }
+  }
+  batcher_u32<VT>(x);
+
+  // ---- warp levels: runs of 16 -> 512 in registers ----
+#pragma unroll
+  for (int m = 1; m <= 5; ++m) {
+    const int g = 1 << m;
+    {  // flip: element e <-> 16g - 1 - e
+      const bool upper = (lane & (g - 1)) >= (g >> 1);
+#pragma unroll
+      for (int q = 0; q < VT / 2; ++q) {
+        const uint32_t a = __shfl_xor_sync(0xffffffffu, x[VT - 1 - q], g - 1);
+        const uint32_t b = __shfl_xor_sync(0xffffffffu, x[q], g - 1);
+        ce_dir(x[q], a, upper);
+        ce_dir(x[VT - 1 - q], b, upper);
+      }
+    }
+#pragma unroll
+    for (int st = g >> 2; st >= 1; st >>= 1) {  // half-cleaners across lanes
+      const bool upper = (lane & st) != 0;
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        ce_dir(x[q], __shfl_xor_sync(0xffffffffu, x[q], st), upper);
+    }
+#pragma unroll
+    for (int st = VT / 2; st >= 1; st >>= 1)  // half-cleaners in registers
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        if ((q & st) == 0)
+          ce_u32(x[q], x[q + st]);
+  }
+
+  // ---- smem Merge Path passes: runs of 512 -> NV ----
+  const int p0 = tid * VT;
+#pragma unroll 1
+  for (int w = 512; w < NV; w *= 2) {
+    {
+      const int r = p0 / w, off = p0 % w;
+      const int o = r * (w + 1) + off;
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        s[pad32(o + q)] = x[q];
+      if (off + VT == w)
+        s[pad32(o + VT)] = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    const int diag = p0 % (2 * w);
+    const int aO = (p0 / (2 * w)) * 2 * (w + 1);
+    const int bO = aO + w + 1;
+    int lo = diag > w ? diag - w : 0;
+    int hi = diag < w ? diag : w;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s[pad32(bO + diag - 1 - mid)] < s[pad32(aO + mid)])
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    int pa = aO + lo, pb = bO + (diag - lo);
+    const int ea = aO + w;
+    uint32_t ka = s[pad32(pa)], kb = s[pad32(pb)];
+#pragma unroll
+    for (int q = 0; q < VT; ++q) {
+      const bool tb = kb < ka;
+      x[q] = tb ? kb : ka;
+      pa = tb ? pa : min(pa + 1, ea);
+      pb = tb ? pb + 1 : pb;
+      const uint32_t nx = s[pad32(tb ? pb : pa)];
+      kb = tb ? nx : kb;
+      ka = tb ? ka : nx;
+    }
+    __syncthreads();
+  }
+
+  // ---- x = sorted positions [p0, p0 + 16) of the block ----
+  if constexpr (ALIGNED) {
+    uint4 *dst = reinterpret_cast<uint4 *>(out + base + p0);
+#pragma unroll
+    for (int m = 0; m < VT / 4; ++m) {
+      uint4 v;
+      v.x = static_cast<uint32_t>(from_order_u32<KT>(x[4 * m + 0]));
+      v.y = static_cast<uint32_t>(from_order_u32<KT>(x[4 * m + 1]));
+      v.z = static_cast<uint32_t>(from_order_u32<KT>(x[4 * m + 2]));
+      v.w = static_cast<uint32_t>(from_order_u32<KT>(x[4 * m + 3]));
+      dst[m] = v;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < VT; ++q)
+      if (p0 + q < cnt)
+        out[base + p0 + q] = from_order_u32<KT>(x[q]);
+  }
+}
+
+}  // namespace mpb

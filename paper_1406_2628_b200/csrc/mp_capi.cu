@@ -164,6 +164,9 @@ constexpr uint64_t kRun = kBlockNT * kBlockVT;  // 2048-key block-sort runs
 constexpr int kBareNT = 256;
 constexpr int kBareVT = 17;  // odd: conflict-free strided smem stores
 constexpr uint64_t kBareRun = kBareNT * kBareVT;
+// bare 32-bit keys, MP_BLOCK_SORT=warp: K3w (mp_bsort.cuh), 4096-key runs
+constexpr int kWarpNT = 256;
+constexpr uint64_t kWarpRun = kWarpNT * 16;
 
 template <class K> cudaError_t set_smem(K kernel, uint32_t bytes) {
   if (bytes <= 48 * 1024)
@@ -519,15 +522,22 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   // MP_BLOCK_SORT=radix: LSD radix block sort for bare 32-bit keys (same
   // bytes).  Opt-in: measured on B200 at 30.0 ms for 2^30 keys vs 8.3 ms for
   // the merge-based block sort (match.any ranking + 1.7 G bank conflicts),
-  // though it issues 35 % fewer instructions.  MP_BLOCK_SORT=merge: the
-  // general merge-based block sort K3 for bare keys too (A/B testing).
+  // though it issues 35 % fewer instructions.
   static const int bs_engine = [] {
     const char *e = std::getenv("MP_BLOCK_SORT");
-    return !e ? 0 : std::strcmp(e, "radix") == 0 ? 1 : std::strcmp(e, "merge") == 0 ? 2 : 0;
+    return !e ? 3
+              : std::strcmp(e, "radix") == 0 ? 1
+              : std::strcmp(e, "merge") == 0 ? 2
+              : std::strcmp(e, "bare") == 0  ? 0
+                                             : 3;
   }();
+  // bare 32-bit keys: K3w by default (B200, 2^30 u32: block sort 7.1 ms vs
+  // 9.0 ms for K3b, whole sort 31.6 vs 33.1 ms); MP_BLOCK_SORT=bare selects
+  // K3b, =merge the stable K3, =radix the LSD radix block sort
   constexpr bool kBare4 = !VALS && sizeof(T) == 4 && KT::kind != kElement;
   const bool use_bare = kBare4 && bs_engine == 0;
-  const uint64_t run0 = use_bare ? kBareRun : kRun;
+  const bool use_warp = kBare4 && bs_engine == 3;  // K3w, 4096-key runs
+  const uint64_t run0 = use_bare ? kBareRun : use_warp ? kWarpRun : kRun;
   int rounds = 0;
   for (uint64_t w = run0; w < n; w *= 2)
     ++rounds;
@@ -553,7 +563,24 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
 
   bool block_sorted = false;
   if constexpr (kBare4) {
-    if (use_bare) {
+    if (use_warp) {
+      constexpr uint32_t smem = warp_sort_smem_bytes<kWarpNT>();
+      const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+      const uint64_t whole = al ? n / kWarpRun : 0, blocks = cdiv(n, kWarpRun);
+      if (whole) {
+        auto kern = block_sort_warp_kernel<KT, kWarpNT, true>;
+        MP_CUDA(set_smem(kern, smem));
+        kern<<<static_cast<unsigned>(whole), kWarpNT, smem, s>>>(in, src, n, 0);
+        MP_LAUNCHED("block_sort_warp_kernel");
+      }
+      if (blocks > whole) {
+        auto kern = block_sort_warp_kernel<KT, kWarpNT, false>;
+        MP_CUDA(set_smem(kern, smem));
+        kern<<<static_cast<unsigned>(blocks - whole), kWarpNT, smem, s>>>(in, src, n, whole);
+        MP_LAUNCHED("block_sort_warp_kernel(tail)");
+      }
+      block_sorted = true;
+    } else if (use_bare) {
       constexpr uint32_t smem = bare_sort_smem_bytes<kBareNT, kBareVT>();
       const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
       const uint64_t whole = al ? n / kBareRun : 0, blocks = cdiv(n, kBareRun);
