@@ -22,7 +22,6 @@
 #include "mp_kernels.cuh"
 #include "mp_spm.cuh"
 #include "mp_pieces.cuh"
-#include "mp_radix.cuh"
 #include "mp_bsort.cuh"
 #include "mp_quad.cuh"
 
@@ -519,21 +518,17 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   uint32_t *auxv = VALS ? reinterpret_cast<uint32_t *>(ws + L.vals_off) : nullptr;
   uint64_t *P = reinterpret_cast<uint64_t *>(ws + L.part_off);
 
-  // MP_BLOCK_SORT=radix: LSD radix block sort for bare 32-bit keys (same
-  // bytes).  Opt-in: measured on B200 at 30.0 ms for 2^30 keys vs 8.3 ms for
-  // the merge-based block sort (match.any ranking + 1.7 G bank conflicts),
-  // though it issues 35 % fewer instructions.
+  // bare 32-bit keys: K3w by default (B200, 2^30 u32: block sort 7.1 ms vs
+  // 9.0 ms for K3b, whole sort 31.6 vs 33.1 ms); MP_BLOCK_SORT=bare selects
+  // K3b, =merge the stable K3.  (An LSD radix block sort with match.any
+  // ranking was measured at 30 ms for the block pass alone and dropped.)
   static const int bs_engine = [] {
     const char *e = std::getenv("MP_BLOCK_SORT");
     return !e ? 3
-              : std::strcmp(e, "radix") == 0 ? 1
               : std::strcmp(e, "merge") == 0 ? 2
               : std::strcmp(e, "bare") == 0  ? 0
                                              : 3;
   }();
-  // bare 32-bit keys: K3w by default (B200, 2^30 u32: block sort 7.1 ms vs
-  // 9.0 ms for K3b, whole sort 31.6 vs 33.1 ms); MP_BLOCK_SORT=bare selects
-  // K3b, =merge the stable K3, =radix the LSD radix block sort
   constexpr bool kBare4 = !VALS && sizeof(T) == 4 && KT::kind != kElement;
   const bool use_bare = kBare4 && bs_engine == 0;
   const bool use_warp = kBare4 && bs_engine == 3;  // K3w, 4096-key runs
@@ -596,15 +591,6 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
         kern<<<static_cast<unsigned>(blocks - whole), kBareNT, smem, s>>>(in, src, n, whole);
         MP_LAUNCHED("block_sort_bare_kernel(tail)");
       }
-      block_sorted = true;
-    } else if (bs_engine == 1) {
-      static_assert(kRadixNV == kRun, "radix block = sort run");
-      constexpr uint32_t smem = radix_smem_bytes();
-      auto kern = block_radix_sort_kernel<KT>;
-      MP_CUDA(set_smem(kern, smem));
-      kern<<<static_cast<unsigned>(cdiv(n, kRun)), kRadixNT, smem, s>>>(in, src,
-                                                                       n);
-      MP_LAUNCHED("block_radix_sort_kernel");
       block_sorted = true;
     }
   }

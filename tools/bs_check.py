@@ -1,5 +1,5 @@
-"""Block-sort A/B: radix vs merge block sort (env MP_BLOCK_SORT=merge in a
-second process), correctness vs torch.sort, and sort timings."""
+"""Block-sort A/B (env MP_BLOCK_SORT=warp|bare|merge, MP_SORT_QUAD=1 in separate
+processes): correctness vs torch.sort and sort timings."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
