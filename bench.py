@@ -56,12 +56,12 @@ CONFIGS = {
     "3b": dict(kind="merge", key="u64", gen=(4, 3), na=1 << 29, nb=1 << 25, bytes_per=24, vals=True,
                desc="config3b: stable merge u64 key + u32 value, |A|=2^29 |B|=2^25, B below A"),
     "4": dict(kind="sort", key="u32", gen=(0, None), n=1 << 30, bytes_per=160,
-              desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 4096-key block sort + 18 rounds"),
+              desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 8192-key block sort + 17 rounds"),
     "5": dict(kind="merge", key="f32", gen=(5, 6), na=1 << 31, nb=1 << 31, bytes_per=8,
               desc="config5: stable merge f32 |A|=|B|=2^31, A~Normal(0,1), B~Exp(1), IEEE "
                    "totalOrder (one GPU: the whole merge; --gpus 8: sharded)"),
 }
-BARE_RUN = 4096  # mp_sort's block-sort run for bare 32-bit keys (K3w: 256 threads x 16)
+BARE_RUN = 8192  # mp_sort's block-sort run for bare 32-bit keys (K3w: 512 threads x 16)
 
 
 def sort_rounds(n: int, run: int = BARE_RUN) -> int:
@@ -243,12 +243,15 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
                                          scratch.data_ptr(), scratch_b, stream.cuda_stream))
                 if evs is not None:
                     evs[1].record(stream)
-            launches_per_step = 2 * sort_rounds(n) + (n >= BARE_RUN) + (n % BARE_RUN > 0)
+            launches_per_step = None  # measured on the first warm-up step
             units = n
 
+        c_w = N.lib.mp_launch_count()
         for _ in range(args.warmup):
             step()
         stream.synchronize()
+        if launches_per_step is None:  # the library's own count for one step
+            launches_per_step = (N.lib.mp_launch_count() - c_w) // max(1, args.warmup)
         barrier(dist_on)
         torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -279,7 +282,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
         kname = "merge_tiles_kernel (K2); step = K1 grid-snapped split search + K2"
     else:
         alg_bytes = n * 8 * (1 + sort_rounds(n))
-        kname = "mp_sort: block_sort_warp + 18 x (round_partition + merge_tiles)"
+        kname = "mp_sort: block_sort_warp + 17 x (round_partition + merge_tiles)"
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     traffic = None
     tpath = ROOT / "profiles" / f"traffic_config{args.config}.json"

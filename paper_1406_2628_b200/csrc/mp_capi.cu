@@ -163,8 +163,11 @@ constexpr uint64_t kRun = kBlockNT * kBlockVT;  // 2048-key block-sort runs
 constexpr int kBareNT = 256;
 constexpr int kBareVT = 17;  // odd: conflict-free strided smem stores
 constexpr uint64_t kBareRun = kBareNT * kBareVT;
-// bare 32-bit keys, MP_BLOCK_SORT=warp: K3w (mp_bsort.cuh), 4096-key runs
-constexpr int kWarpNT = 256;
+// bare 32-bit keys: K3w (mp_bsort.cuh), 16 keys per thread
+#ifndef MP_WARP_NT
+#define MP_WARP_NT 512  // 8192-key runs: one round fewer (17 at 2^30) for
+#endif                  // one more smem pass; B200 2^30 u32 31.52 -> 31.36 ms
+constexpr int kWarpNT = MP_WARP_NT;
 constexpr uint64_t kWarpRun = kWarpNT * 16;
 
 template <class K> cudaError_t set_smem(K kernel, uint32_t bytes) {
@@ -531,7 +534,7 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   }();
   constexpr bool kBare4 = !VALS && sizeof(T) == 4 && KT::kind != kElement;
   const bool use_bare = kBare4 && bs_engine == 0;
-  const bool use_warp = kBare4 && bs_engine == 3;  // K3w, 4096-key runs
+  const bool use_warp = kBare4 && bs_engine == 3;  // K3w, kWarpRun-key runs
   const uint64_t run0 = use_bare ? kBareRun : use_warp ? kWarpRun : kRun;
   int rounds = 0;
   for (uint64_t w = run0; w < n; w *= 2)

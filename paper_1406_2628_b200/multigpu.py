@@ -758,7 +758,7 @@ def bench_distributed_sort(args, cfg, ws, rank, local, clock=None):
     el = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=red_dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     del ho
-    rounds, w = 0, 4096  # mp_sort's bare 32-bit block-sort run
+    rounds, w = 0, 8192  # mp_sort's bare 32-bit block-sort run
     while w < (n + ws - 1) // ws:
         w, rounds = 2 * w, rounds + 1
     passes = 1 + rounds + (ws - 1).bit_length()

@@ -613,7 +613,7 @@ print("FUSED OK")
 @pytest.mark.parametrize("S", ("u32", "i32", "f32"))
 @pytest.mark.parametrize("engine,quad", [("warp", "0"), ("bare", "0"), ("bare", "1")])
 def test_fused_round_sorts_vs_oracle(cuda, S, engine, quad):
-    """Bare 32-bit sorts through each block sort -- K3w (default, 4096-key
+    """Bare 32-bit sorts through each block sort -- K3w (default, 8192-key
     runs, warp-level bitonic levels) and K3b (4352-key runs) -- then plain
     rounds or, after K3b, fused two-round passes (MP_SORT_QUAD=1,
     mp_quad.cuh).  The switches are read once per process, hence the
@@ -630,7 +630,7 @@ def test_fused_round_sorts_vs_oracle(cuda, S, engine, quad):
 
 
 def _fused_round_cases(cuda, S):
-    """Sizes straddle run and group boundaries (runs of 4096 and 4352,
+    """Sizes straddle run and group boundaries (runs of 8192 and 4352,
     groups of 4 runs) so the short last group has 1, 2 or 3 runs; inputs
     include heavy duplicates, all-equal, descending and (f32) signed zeros /
     NaNs."""
@@ -638,8 +638,8 @@ def _fused_round_cases(cuda, S):
     from paper_1406_2628_b200 import mergepath as mp
     port = bindings.port()
     rng = np.random.default_rng(29)
-    sizes = (511, 512, 513, 4095, 4096, 4097, 200_003, 1_000_000)
-    for R in (4096, 4352):
+    sizes = (511, 512, 513, 4095, 4096, 4097, 8191, 8193, 200_003, 1_000_000)
+    for R in (8192, 4352):
         sizes += (4 * R - 1, 4 * R, 4 * R + 1, 5 * R + 7, 6 * R, 7 * R + 3, 16 * R + 1,
                   16 * R + 9 * R, 64 * R - 5)
     for n in sizes:
