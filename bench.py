@@ -57,7 +57,7 @@ CONFIGS = {
                desc="config3b: stable merge u64 key + u32 value, |A|=2^29 |B|=2^25, B below A"),
     "4": dict(kind="sort", key="u32", gen=(0, None), n=1 << 30, bytes_per=160,
               desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 8192-key block sort + 17 rounds"),
-    "5": dict(kind="merge", key="f32", gen=(5, 6), na=1 << 31, nb=1 << 31, bytes_per=8,
+    "5": dict(kind="merge", key="f32", gen=(5, 6), na=1 << 31, nb=1 << 31, bytes_per=8, sharded=True,
               desc="config5: stable merge f32 |A|=|B|=2^31, A~Normal(0,1), B~Exp(1), IEEE "
                    "totalOrder (one GPU: the whole merge; --gpus 8: sharded)"),
 }

@@ -618,9 +618,10 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    kt = {"u32": N.KEY_U32, "i32": N.KEY_I32, "u64": N.KEY_U64, "i64": N.KEY_I64}[cfg["key"]]
-    dt = {"u32": torch.uint32, "i32": torch.int32, "u64": torch.uint64,
-          "i64": torch.int64}[cfg["key"]]
+    kt = {"u32": N.KEY_U32, "i32": N.KEY_I32, "f32": N.KEY_F32, "u64": N.KEY_U64,
+          "i64": N.KEY_I64}[cfg["key"]]
+    dt = {"u32": torch.uint32, "i32": torch.int32, "f32": torch.float32,
+          "u64": torch.uint64, "i64": torch.int64}[cfg["key"]]
     st = torch.cuda.current_stream().cuda_stream
 
     def gen(kind, seed, n, first):
@@ -632,10 +633,19 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
     # MP_BENCH_SCALE=k shrinks the per-GPU sizes by 2^k (multi-rank smoke
     # tests on a one-GPU box); reductions go through the backend's device
     shrink = int(os.environ.get("MP_BENCH_SCALE", "0"))
-    na, nb = cfg["na"] >> shrink, cfg["nb"] >> shrink
+    # config 5 fixes the global sizes (sharded over the ranks: strong
+    # scaling); the others fix the per-GPU sizes (weak scaling)
+    strong = bool(cfg.get("sharded"))
+    NA, NB = cfg["na"] >> shrink, cfg["nb"] >> shrink
+    if strong:
+        a0, a1 = rank * NA // ws, (rank + 1) * NA // ws
+        b0, b1 = rank * NB // ws, (rank + 1) * NB // ws
+    else:
+        a0, a1, b0, b1 = rank * NA, (rank + 1) * NA, rank * NB, (rank + 1) * NB
+    na, nb = a1 - a0, b1 - b0
     red_dev = dev if dist.get_backend() == "nccl" else torch.device("cpu")
-    a, _ = sharded_sort(gen(cfg["gen"][0], 1, na, rank * na), key_type=kt)
-    b, _ = sharded_sort(gen(cfg["gen"][1], 2, nb, rank * nb), key_type=kt)
+    a, _ = sharded_sort(gen(cfg["gen"][0], 1, na, a0), key_type=kt)
+    b, _ = sharded_sort(gen(cfg["gen"][1], 2, nb, b0), key_type=kt)
     a, b = a.contiguous(), b.contiguous()
     transport = getattr(args, "transport", "p2p")
     if transport == "p2p":
@@ -663,7 +673,7 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
     ms = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    total = (na + nb) * ws
+    total = (NA + NB) if strong else (na + nb) * ws
     value = total * args.steps / (ms / 1e3)
     # e2e through the public API with host buffers: H2D shard, sharded merge,
     # D2H of this rank's output slice (wall clock, max over ranks)
@@ -689,10 +699,12 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
     return {
         "metric": "merged elements/s", "value": value, "unit": "elements/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": cfg["key"],
         "data": "synthetic: SplitMix64 counter generator, globally sorted with sharded_sort",
-        "config": {"workload": cfg["desc"] + f" per GPU; global |A|={na * ws} |B|={nb * ws}",
+        "config": {"workload": cfg["desc"] + (f"; sharded over {ws} GPUs" if strong else
+                                             f" per GPU; global |A|={NA * ws} |B|={NB * ws}"),
                    "parallelism": f"merge-path diagonal split over {ws} GPUs ("
                                   + ("NVLink pull fused into the merge kernels via CUDA IPC"
                                      if transport == "p2p" else "NCCL all_to_all exchange") + ")",

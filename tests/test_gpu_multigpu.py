@@ -234,3 +234,25 @@ def test_peer_lsu_loader_subprocess(cuda):
                        timeout=900, env=dict(os.environ, MP_PEER_LSU="1"), cwd=str(ROOT))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("config", ["2", "4", "5"])
+def test_distributed_bench_two_ranks(cuda, config):
+    """bench.py --gpus 2 through torchrun (both ranks on the box's one GPU,
+    gloo plumbing, inputs shrunk 2^5): the fused P2P merge (config 2, weak
+    scaling; config 5, f32, the fixed global size sharded) and the P2P sort
+    (config 4) run and print one JSON line with the library's launch count."""
+    import json
+    import subprocess
+    env = dict(os.environ, MP_BENCH_DEVICE="0", MP_BENCH_BACKEND="gloo", MP_BENCH_SCALE="5")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(_free_port()), "bench.py", "--config", config, "--gpus", "2",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True,
+                       timeout=600, env=env, cwd=str(ROOT))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["scaling"] == ("weak" if config == "2" else "strong")
