@@ -647,12 +647,23 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
     a, _ = sharded_sort(gen(cfg["gen"][0], 1, na, a0), key_type=kt)
     b, _ = sharded_sort(gen(cfg["gen"][1], 2, nb, b0), key_type=kt)
     a, b = a.contiguous(), b.contiguous()
+    av = bv = None
+    if cfg.get("vals"):
+        # config 3 payload: each key's index in its globally sorted array
+        # (bit 31 set on B's), as in the single-GPU bench
+        comm = _Comm()
+        la = [x[0] for x in comm.all_gather_int([a.numel()])]
+        lb = [x[0] for x in comm.all_gather_int([b.numel()])]
+        av = (torch.arange(a.numel(), dtype=torch.int64, device=dev) + sum(la[:rank])
+              ).to(torch.int32).view(torch.uint32)
+        bv = ((torch.arange(b.numel(), dtype=torch.int64, device=dev) + sum(lb[:rank]))
+              | (1 << 31)).to(torch.int32).view(torch.uint32)
     transport = getattr(args, "transport", "p2p")
     if transport == "p2p":
-        merger = P2PMerger(a, b, key_type=kt)  # IPC mappings built once (untimed)
+        merger = P2PMerger(a, b, av, bv, key_type=kt)  # IPC mappings built once (untimed)
         step = lambda: merger()  # noqa: E731
     else:
-        step = lambda: sharded_merge(a, b, key_type=kt)  # noqa: E731
+        step = lambda: sharded_merge(a, b, av, bv, key_type=kt)  # noqa: E731
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -678,18 +689,25 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
     # e2e through the public API with host buffers: H2D shard, sharded merge,
     # D2H of this rank's output slice (wall clock, max over ranks)
     ha, hb = a.cpu().pin_memory(), b.cpu().pin_memory()
+    hav = av.cpu().pin_memory() if av is not None else None
+    hbv = bv.cpu().pin_memory() if bv is not None else None
     e2e_steps = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
     dist.barrier()
     t = time.perf_counter()
     for _ in range(e2e_steps):
         a.copy_(ha, non_blocking=True)  # H2D into the registered shards
         b.copy_(hb, non_blocking=True)
-        o, _ = step()
+        if hav is not None:
+            av.copy_(hav, non_blocking=True)
+            bv.copy_(hbv, non_blocking=True)
+        o, ov = step()
         ho = o.cpu()
+        if ov is not None:
+            ho = ov.cpu()
     torch.cuda.synchronize()
     el = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=red_dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    ks = a.element_size()
+    ks = a.element_size() + (4 if av is not None else 0)  # key (+ value) bytes
     peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json")
                       .read_text())["hbm_gbs"] if (Path(__file__).resolve().parents[1] /
                                                    "MEASURED_PEAKS.json").exists() else 6650.0

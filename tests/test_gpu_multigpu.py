@@ -236,12 +236,13 @@ def test_peer_lsu_loader_subprocess(cuda):
     assert " passed" in r.stdout
 
 
-@pytest.mark.parametrize("config", ["2", "4", "5"])
+@pytest.mark.parametrize("config", ["2", "3a", "4", "5"])
 def test_distributed_bench_two_ranks(cuda, config):
     """bench.py --gpus 2 through torchrun (both ranks on the box's one GPU,
     gloo plumbing, inputs shrunk 2^5): the fused P2P merge (config 2, weak
     scaling; config 5, f32, the fixed global size sharded) and the P2P sort
-    (config 4) run and print one JSON line with the library's launch count."""
+    (config 4) run and print one JSON line with the library's launch count;
+    config 3a carries its u32 values through the fused merge."""
     import json
     import subprocess
     env = dict(os.environ, MP_BENCH_DEVICE="0", MP_BENCH_BACKEND="gloo", MP_BENCH_SCALE="5")
@@ -255,4 +256,4 @@ def test_distributed_bench_two_ranks(cuda, config):
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
-    assert d["scaling"] == ("weak" if config == "2" else "strong")
+    assert d["scaling"] == ("weak" if config in ("2", "3a") else "strong")
