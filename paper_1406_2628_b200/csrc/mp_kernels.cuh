@@ -454,12 +454,23 @@ constexpr int block_sort_min_blocks() {
 
 // Interior copy by the LSU: 16-byte vector loads, all threads (the peer-
 // memory loader: NVLink reads of mapped peer pointers are plain LDG.128).
+// Four loads are issued before their stores so each thread keeps four
+// NVLink reads in flight (peer LDG latency is ~1 us; B300_MICROARCH.md).
 template <int NT>
 __device__ __forceinline__ void lsu_copy16(char *smem, const char *g, uint32_t bytes,
                                            int tid) {
   const uint4 *src = reinterpret_cast<const uint4 *>(g);
   uint4 *dst = reinterpret_cast<uint4 *>(smem);
-  for (uint32_t q = tid; q < bytes / 16; q += NT)
+  const uint32_t n = bytes / 16;
+  uint32_t q = tid;
+  for (; q + 3 * NT < n; q += 4 * NT) {
+    const uint4 v0 = src[q], v1 = src[q + NT], v2 = src[q + 2 * NT], v3 = src[q + 3 * NT];
+    dst[q] = v0;
+    dst[q + NT] = v1;
+    dst[q + 2 * NT] = v2;
+    dst[q + 3 * NT] = v3;
+  }
+  for (; q < n; q += NT)
     dst[q] = src[q];
 }
 
