@@ -716,3 +716,81 @@ def test_beyond_2_32_elements(cuda):
     hb, sb = fingerprint(b)
     ho, so = fingerprint(out)
     assert so == sa + sb and torch.equal(ho, ha + hb)
+
+
+def _ref_or_skip():
+    from oracle import bindings as B
+    if not B.REF_LIB.exists():
+        pytest.skip("oracle/_ref (the reference library) not built")
+    return B
+
+
+@pytest.mark.parametrize("config", ["2", "3a", "3b"])
+def test_full_size_bit_exact_vs_reference(cuda, config):
+    """BASELINE configs 2 and 3 at full size, byte for byte against the
+    REFERENCE itself (oracle/_ref: parallel_merge_into on this host's cores)
+    on the same input bytes: keys, and for config 3 the {key, value}
+    records (values = source index, bit 31 marks B)."""
+    torch = _torch()
+    B = _ref_or_skip()
+    from paper_1406_2628_b200 import mergepath as mp
+    R = B.ref()
+    team = R.team(B.host_cores())
+    if config == "2":
+        n = 1 << 28
+        a = _sorted_dev(1, 1, n, cuda)
+        b = _sorted_dev(1, 2, n, cuda)
+        got = mp.parallel_merge(a, b, 8).cpu().numpy()
+        want, _, _ = R.merge("i32", a.cpu().numpy(), b.cpu().numpy(), team=team)
+        team.close()
+        assert np.array_equal(got, want)
+        return
+    na, nb = 1 << 29, 1 << 25
+    ka, kb = ((2, 2) if config == "3a" else (4, 3))
+    a = _sorted_dev(ka, 1, na, cuda)
+    b = _sorted_dev(kb, 2, nb, cuda)
+    av = torch.arange(na, dtype=torch.int32, device=cuda).view(torch.uint32)
+    bv = (torch.arange(nb, dtype=torch.int32, device=cuda)
+          + torch.iinfo(torch.int32).min).view(torch.uint32)
+    out, outv = mp.parallel_merge(a, b, 8, a_vals=av, b_vals=bv)
+    ra = np.zeros(na, dtype=B.KV_DTYPE)
+    ra["key"], ra["val"] = a.cpu().numpy(), av.cpu().numpy()
+    rb = np.zeros(nb, dtype=B.KV_DTYPE)
+    rb["key"], rb["val"] = b.cpu().numpy(), bv.cpu().numpy()
+    del a, b, av, bv
+    want, _, _ = R.merge("kv", ra, rb, team=team)
+    team.close()
+    del ra, rb
+    assert np.array_equal(out.cpu().numpy(), want["key"])
+    assert np.array_equal(outv.cpu().numpy(), want["val"])
+
+
+def test_config5_full_size_bit_exact_vs_reference(cuda):
+    """Config 5 on one GPU at full size (f32, |A| = |B| = 2^31, A ~ Normal,
+    B ~ Exp, IEEE totalOrder), byte for byte against the reference's
+    parallel merge with a totalOrder comparator on the same bytes."""
+    torch = _torch()
+    B = _ref_or_skip()
+    from paper_1406_2628_b200 import _native as N
+    st = torch.cuda.current_stream().cuda_stream
+    n = 1 << 31
+    ab = []
+    for kind, seed in ((5, 1), (6, 2)):
+        x = torch.empty(n, dtype=torch.float32, device=cuda)
+        N.check(N.lib.mp_generate(kind, seed, 0, n, x.data_ptr(), st))
+        N.check(N.lib.mp_sort(N.KEY_F32, x.data_ptr(), None, n, None, 0, st))
+        ab.append(x)
+    a, b = ab
+    out = torch.empty(2 * n, dtype=torch.float32, device=cuda)
+    N.check(N.lib.mp_merge(N.KEY_F32, a.data_ptr(), None, n, b.data_ptr(), None, n,
+                           out.data_ptr(), None, st))
+    torch.cuda.synchronize()
+    ha, hb = a.cpu().numpy(), b.cpu().numpy()
+    del a, b
+    got = out.cpu().numpy()
+    del out
+    R = B.ref()
+    team = R.team(B.host_cores())
+    want, _, _ = R.merge("f32", ha, hb, team=team)
+    team.close()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
