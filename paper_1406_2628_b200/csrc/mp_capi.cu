@@ -491,6 +491,83 @@ template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
   return L;
 }
 
+// bare 32-bit keys: K3w by default (B200, 2^30 u32: block sort 7.1 ms vs
+// 9.0 ms for K3b, whole sort 31.6 vs 33.1 ms); MP_BLOCK_SORT=bare selects
+// K3b, =merge the stable K3.  (An LSD radix block sort with match.any
+// ranking was measured at 30 ms for the block pass alone and dropped.)
+int block_sort_engine() {
+  static const int e = [] {
+    const char *v = std::getenv("MP_BLOCK_SORT");
+    return !v ? 3
+              : std::strcmp(v, "merge") == 0 ? 2
+              : std::strcmp(v, "bare") == 0  ? 0
+                                             : 3;
+  }();
+  return e;
+}
+
+// Run length the block sort leaves and the round tile (mp_sort's schedule).
+template <class KT, bool VALS> uint64_t sort_run0() {
+  constexpr bool bare4 = !VALS && sizeof(typename KT::T) == 4 && KT::kind != kElement;
+  if (bare4 && block_sort_engine() == 0)
+    return kBareRun;
+  if (bare4 && block_sort_engine() == 3)
+    return kWarpRun;
+  return kRun;
+}
+template <class KT, bool VALS> uint32_t sort_round_tile() {
+  return sort_run0<KT, VALS>() == kBareRun ? static_cast<uint32_t>(kBareRun)
+                                           : SortMergeCfg<KT>::TILE;
+}
+
+// Plain bottom-up rounds over sorted runs of width w0 held in `src`
+// (sort.hpp:71-128): per round K4 (pair-local split points at tile NV) and
+// K2 over RoundMap, ping-pong src <-> dst.  *res / *resv receive the buffer
+// holding the result.
+template <class KT, bool VALS>
+int sort_rounds_from(typename KT::T *src, uint32_t *srcv, typename KT::T *dst,
+                     uint32_t *dstv, uint64_t n, uint64_t w0, uint32_t NV,
+                     uint64_t *P, cudaStream_t s, typename KT::T **res,
+                     uint32_t **resv) {
+  using T = typename KT::T;
+  constexpr int NT = SortMergeCfg<KT>::NT, VT = SortMergeCfg<KT>::VT;
+  const uint64_t tiles = cdiv(n, NV);
+  constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
+  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, RoundMap, false>;
+  MP_CUDA(set_smem(kern, smem));
+  uint32_t tshift = static_cast<uint32_t>(__builtin_ctzll(2 * w0 / NV));  // 2w = NV << tshift
+  for (uint64_t w = w0; w < n; w *= 2, ++tshift) {
+    // K4 || K2 within the round (the round's input is complete)
+    auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
+      if (hi <= lo)
+        return MP_OK;
+      round_partition_kernel<KT>
+          <<<static_cast<unsigned>(cdiv(hi - lo, 128)), 128, 0, st>>>(
+              src, n, w, tshift, NV, hi, P, lo);
+      MP_LAUNCHED("round_partition_kernel");
+      return MP_OK;
+    };
+    auto tile = [&](uint64_t t0, uint64_t t1, cudaStream_t st) -> int {
+      if (t1 <= t0)
+        return MP_OK;
+      kern<<<static_cast<unsigned>(t1 - t0), NT, smem, st>>>(
+          RoundMap{P, n, w, NV, tshift}, src, srcv, src, srcv, dst, dstv,
+          nullptr, t0);
+      MP_LAUNCHED("merge_tiles_kernel(round)");
+      return MP_OK;
+    };
+    if (int rc = run_overlapped(tiles, tiles, split, tile, s))
+      return rc;
+    std::swap(src, dst);
+    std::swap(srcv, dstv);
+  }
+  if (res)
+    *res = src;
+  if (resv)
+    *resv = srcv;
+  return MP_OK;
+}
+
 template <class KT, bool VALS>
 int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
               uint32_t *vals, uint64_t n, void *scratch,
@@ -521,17 +598,7 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   uint32_t *auxv = VALS ? reinterpret_cast<uint32_t *>(ws + L.vals_off) : nullptr;
   uint64_t *P = reinterpret_cast<uint64_t *>(ws + L.part_off);
 
-  // bare 32-bit keys: K3w by default (B200, 2^30 u32: block sort 7.1 ms vs
-  // 9.0 ms for K3b, whole sort 31.6 vs 33.1 ms); MP_BLOCK_SORT=bare selects
-  // K3b, =merge the stable K3.  (An LSD radix block sort with match.any
-  // ranking was measured at 30 ms for the block pass alone and dropped.)
-  static const int bs_engine = [] {
-    const char *e = std::getenv("MP_BLOCK_SORT");
-    return !e ? 3
-              : std::strcmp(e, "merge") == 0 ? 2
-              : std::strcmp(e, "bare") == 0  ? 0
-                                             : 3;
-  }();
+  const int bs_engine = block_sort_engine();
   constexpr bool kBare4 = !VALS && sizeof(T) == 4 && KT::kind != kElement;
   const bool use_bare = kBare4 && bs_engine == 0;
   const bool use_warp = kBare4 && bs_engine == 3;  // K3w, kWarpRun-key runs
@@ -612,77 +679,39 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   static_assert(NT * VT >= int(SortMergeCfg<KT>::TILE) && (2 * kRun) % SortMergeCfg<KT>::TILE == 0 &&
                     (!kBare4 || NT * VT >= int(kBareRun)),
                 "round tile shape");
-  const uint32_t NV = use_bare ? static_cast<uint32_t>(kBareRun) : SortMergeCfg<KT>::TILE;
-  const uint64_t tiles = cdiv(n, NV);
-  constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
-  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, RoundMap, false>;
-  MP_CUDA(set_smem(kern, smem));
-  uint32_t tshift = static_cast<uint32_t>(__builtin_ctzll(2 * run0 / NV));  // 2w = NV << tshift
-  int fused_left = quad_passes;
-  for (uint64_t w = run0; w < n; w *= 2, ++tshift) {
-    if constexpr (kBare4) {
-      if (fused_left > 0) {
-        // rounds (w, 2w) in one pass: K4q crossings + K5q segment merges
-        --fused_left;
-        QuadPt *QP = reinterpret_cast<QuadPt *>(ws + L.quad_off);
-        const uint32_t G = static_cast<uint32_t>(kQuadG);
-        const uint32_t lshift = static_cast<uint32_t>(__builtin_ctzll(4 * w / G));
-        const uint64_t full = n / (4 * w);
-        uint64_t lines = full << lshift;
-        if (full * 4 * w < n) {  // short last group
-          const uint64_t S = full * 4 * w;
-          uint64_t l[4];
-          for (int r = 0; r < 4; ++r) {
-            const uint64_t st = S + r * w;
-            l[r] = st < n ? std::min<uint64_t>(w, n - st) : 0;
-          }
-          lines += cdiv(l[0] + l[1], G) + cdiv(l[2] + l[3], G);
+  const uint32_t NV = sort_round_tile<KT, VALS>();
+  uint64_t w = run0;
+  if constexpr (kBare4) {
+    for (int fused_left = quad_passes; fused_left > 0 && w < n; --fused_left, w *= 4) {
+      // rounds (w, 2w) in one pass: K4q crossings + K5q segment merges
+      QuadPt *QP = reinterpret_cast<QuadPt *>(ws + L.quad_off);
+      const uint32_t G = static_cast<uint32_t>(kQuadG);
+      const uint32_t lshift = static_cast<uint32_t>(__builtin_ctzll(4 * w / G));
+      const uint64_t full = n / (4 * w);
+      uint64_t lines = full << lshift;
+      if (full * 4 * w < n) {  // short last group
+        const uint64_t S = full * 4 * w;
+        uint64_t l[4];
+        for (int r = 0; r < 4; ++r) {
+          const uint64_t st = S + r * w;
+          l[r] = st < n ? std::min<uint64_t>(w, n - st) : 0;
         }
-        quad_partition_kernel<KT, kQuadG><<<static_cast<unsigned>(cdiv(lines, 128)), 128, 0, s>>>(
-            src, n, w, lshift, lines, QP);
-        MP_LAUNCHED("quad_partition_kernel");
-        constexpr int QNT = 2 * NT / MP_QUAD_DIV, QVT = VT;
-        static_assert(QNT / 2 * QVT >= int(kQuadG), "inner merges fit half a CTA");
-        constexpr uint32_t qsmem = merge_smem_bytes<KT, false, QNT, QVT>();
-        auto qkern = quad_merge_kernel<KT, QNT, QVT, kQuadG>;
-        MP_CUDA(set_smem(qkern, qsmem));
-        qkern<<<static_cast<unsigned>(lines), QNT, qsmem, s>>>(src, dst, n, w, lshift, QP);
-        MP_LAUNCHED("quad_merge_kernel");
-        std::swap(src, dst);
-        w *= 2;  // the loop's own doubling completes the second round
-        ++tshift;
-        continue;
+        lines += cdiv(l[0] + l[1], G) + cdiv(l[2] + l[3], G);
       }
+      quad_partition_kernel<KT, kQuadG><<<static_cast<unsigned>(cdiv(lines, 128)), 128, 0, s>>>(
+          src, n, w, lshift, lines, QP);
+      MP_LAUNCHED("quad_partition_kernel");
+      constexpr int QNT = 2 * NT / MP_QUAD_DIV, QVT = VT;
+      static_assert(QNT / 2 * QVT >= int(kQuadG), "inner merges fit half a CTA");
+      constexpr uint32_t qsmem = merge_smem_bytes<KT, false, QNT, QVT>();
+      auto qkern = quad_merge_kernel<KT, QNT, QVT, kQuadG>;
+      MP_CUDA(set_smem(qkern, qsmem));
+      qkern<<<static_cast<unsigned>(lines), QNT, qsmem, s>>>(src, dst, n, w, lshift, QP);
+      MP_LAUNCHED("quad_merge_kernel");
+      std::swap(src, dst);
     }
-    // K4 || K2 within the round (the round's input is complete)
-    auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
-      if (hi <= lo)
-        return MP_OK;
-      round_partition_kernel<KT>
-          <<<static_cast<unsigned>(cdiv(hi - lo, 128)), 128, 0, st>>>(
-              src, n, w, tshift, NV, hi, P, lo);
-      MP_LAUNCHED("round_partition_kernel");
-      return MP_OK;
-    };
-    auto tile = [&](uint64_t t0, uint64_t t1, cudaStream_t st) -> int {
-      if (t1 <= t0)
-        return MP_OK;
-      kern<<<static_cast<unsigned>(t1 - t0), NT, smem, st>>>(
-          RoundMap{P, n, w, NV, tshift}, src, srcv, src, srcv, dst, dstv,
-          nullptr, t0);
-      MP_LAUNCHED("merge_tiles_kernel(round)");
-      return MP_OK;
-    };
-    if (int rc = run_overlapped(tiles, tiles, split, tile, s))
-      return rc;
-    T *t = src;
-    src = dst;
-    dst = t;
-    uint32_t *tv = srcv;
-    srcv = dstv;
-    dstv = tv;
   }
-  return MP_OK;
+  return sort_rounds_from<KT, VALS>(src, srcv, dst, dstv, n, w, NV, P, s, nullptr, nullptr);
 }
 
 // ---- generators -------------------------------------------------------------
@@ -1679,6 +1708,93 @@ int mp_merge_checksum_host(int kt, const void *a, uint64_t na, const void *b,
   return MP_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Host-buffer sort, pipelined over PCIe: the input is copied in chunks of
+// C = 2^k block runs (~64 MiB) and each chunk is sorted on the device (the
+// full mp_sort) while the next one is in flight -- a chunk-local sort leaves
+// exactly the state the global bottom-up schedule has after log2(C/run)
+// rounds (every aligned C-group sorted; stable within the group) -- then
+// the remaining rounds run over the whole array and the result is copied
+// out.  B200, 2^30 u32 keys: see DESIGN.md.
+template <class KT, bool VALS>
+int sort_host_pipelined(const void *keys_, const uint32_t *vals, uint64_t n,
+                        void *out_keys, uint32_t *out_vals, int device,
+                        bool *done) {
+  using T = typename KT::T;
+  constexpr uint64_t ks = sizeof(T);
+  *done = false;
+  const uint64_t run0 = sort_run0<KT, VALS>();
+  if (run0 & (run0 - 1))
+    return MP_OK;  // non-power-of-two runs (K3b): plain path
+  uint64_t C = run0;
+  while (C * 2 * ks <= (64ull << 20))
+    C *= 2;
+  if (n < 4 * C)
+    return MP_OK;  // too small to pipeline: plain path
+  HostPipe &hp = host_pipe(device);
+  std::lock_guard<std::mutex> lk(hp.mu);
+  if (int rc = hp.setup())
+    return rc;
+  const T *keys = static_cast<const T *>(keys_);
+  auto up = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  const uint32_t NV = sort_round_tile<KT, VALS>();
+  const SortLayout Lc = sort_layout<KT>(VALS, C);
+  const uint64_t o_d = 0, o_aux = up(n * ks);
+  const uint64_t o_dv = o_aux + up(n * ks);
+  const uint64_t o_auxv = o_dv + (VALS ? up(n * 4) : 0);
+  const uint64_t o_P = o_auxv + (VALS ? up(n * 4) : 0);
+  const uint64_t o_cs = o_P + up((cdiv(n, NV) + 1) * 8);
+  ScratchGuard g;
+  if (int rc = alloc_scratch(g, o_cs + Lc.total, hp.cmp))
+    return rc;
+  char *base = static_cast<char *>(g.p);
+  T *d = reinterpret_cast<T *>(base + o_d), *aux = reinterpret_cast<T *>(base + o_aux);
+  uint32_t *dv = VALS ? reinterpret_cast<uint32_t *>(base + o_dv) : nullptr;
+  uint32_t *auxv = VALS ? reinterpret_cast<uint32_t *>(base + o_auxv) : nullptr;
+  uint64_t *P = reinterpret_cast<uint64_t *>(base + o_P);
+  char *cs = base + o_cs;
+  const uint64_t chunks = cdiv(n, C);
+  for (uint64_t c = 0; c < chunks; ++c) {
+    const int sl = static_cast<int>(c % kSlots);
+    const uint64_t off = c * C, len = std::min<uint64_t>(C, n - off);
+    MP_CUDA(cudaMemcpyAsync(d + off, keys + off, len * ks, cudaMemcpyHostToDevice, hp.h2d));
+    if (VALS)
+      MP_CUDA(cudaMemcpyAsync(dv + off, vals + off, len * 4, cudaMemcpyHostToDevice, hp.h2d));
+    MP_CUDA(cudaEventRecord(hp.ev_h2d[sl], hp.h2d));
+    MP_CUDA(cudaStreamWaitEvent(hp.cmp, hp.ev_h2d[sl], 0));
+    if (int rc = sort_impl<KT, VALS>(d + off, VALS ? dv + off : nullptr, d + off,
+                                     VALS ? dv + off : nullptr, len, cs, Lc.total, hp.cmp))
+      return rc;
+  }
+  T *res = nullptr;
+  uint32_t *resv = nullptr;
+  if (int rc = sort_rounds_from<KT, VALS>(d, dv, aux, auxv, n, C, NV, P, hp.cmp, &res, &resv))
+    return rc;
+  MP_CUDA(cudaMemcpyAsync(out_keys, res, n * ks, cudaMemcpyDeviceToHost, hp.cmp));
+  if (VALS)
+    MP_CUDA(cudaMemcpyAsync(out_vals, resv, n * 4, cudaMemcpyDeviceToHost, hp.cmp));
+  MP_CUDA(cudaStreamSynchronize(hp.cmp));
+  *done = true;
+  return MP_OK;
+}
+
+template <class KT> struct SortHostOp {
+  static int run(const void *keys, const uint32_t *vals, uint64_t n,
+                 void *out_keys, uint32_t *out_vals, int device, bool *done) {
+    if (vals) {
+      if (KT::kind == kElement)
+        return fail(MP_ERR_UNSUPPORTED, "ELEMENT keys carry their own tag");
+      return sort_host_pipelined<KT, true>(keys, vals, n, out_keys, out_vals, device, done);
+    }
+    return sort_host_pipelined<KT, false>(keys, nullptr, n, out_keys, nullptr, device, done);
+  }
+};
+}  // namespace
+
+extern "C" {
+
 int mp_sort_host(int kt, const void *keys, const uint32_t *vals, uint64_t n,
                  void *out_keys, uint32_t *out_vals, int device) {
   g_err.clear();
@@ -1692,6 +1808,18 @@ int mp_sort_host(int kt, const void *keys, const uint32_t *vals, uint64_t n,
   DeviceScope ds(device);
   if (ds.err != cudaSuccess)
     return cuda_fail(ds.err, "cudaSetDevice");
+  static const bool pipe_env = [] {
+    const char *e = std::getenv("MP_SORT_HOST_PIPE");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  if (pipe_env && (reinterpret_cast<uintptr_t>(keys) % ks) == 0 &&
+      (reinterpret_cast<uintptr_t>(out_keys) % ks) == 0) {
+    bool done = false;
+    if (int rc = dispatch<SortHostOp>(kt, keys, vals, n, out_keys, out_vals, device, &done))
+      return rc;
+    if (done)
+      return MP_OK;
+  }
   cudaStream_t s = host_stream(device);
   const uint64_t kb = (n * ks + 255) & ~uint64_t(255);
   const uint64_t vb = vals ? ((n * 4 + 255) & ~uint64_t(255)) : 0;

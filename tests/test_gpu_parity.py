@@ -794,3 +794,35 @@ def test_config5_full_size_bit_exact_vs_reference(cuda):
     want, _, _ = R.merge("f32", ha, hb, team=team)
     team.close()
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("S,n", [("u32", (1 << 26) + 12345), ("f32", (1 << 26) + 7),
+                                 ("u64", (1 << 25) + 999)])
+def test_host_sort_pipelined(cuda, S, n):
+    """mp_sort_host over PCIe in chunks (each chunk sorted on the device
+    while the next is copied in, then the remaining rounds): sizes of >= 4
+    chunks, duplicates; u64 carries values to check stability."""
+    from paper_1406_2628_b200 import _native as N
+    rng = np.random.default_rng(31)
+    kt = key_type(S)
+    if S == "u64":
+        x = rng.integers(0, 1 << 20, n, dtype=np.uint64)
+        v = np.arange(n, dtype=np.uint32)
+        out = np.empty_like(x)
+        outv = np.empty_like(v)
+        N.check(N.lib.mp_sort_host(kt, x.ctypes.data, v.ctypes.data, n, out.ctypes.data,
+                                   outv.ctypes.data, 0))
+        perm = np.argsort(x, kind="stable")
+        assert np.array_equal(out, x[perm]) and np.array_equal(outv, v[perm])
+        return
+    x = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    x[::5] = 77
+    if S == "f32":
+        x[1::97] = 0x80000000  # -0.0 among the keys
+    out = np.empty_like(x)
+    N.check(N.lib.mp_sort_host(kt, x.ctypes.data, None, n, out.ctypes.data, None, 0))
+    if S == "u32":
+        assert np.array_equal(out, np.sort(x))
+    else:
+        img = np.where(x & 0x80000000, ~x, x | 0x80000000).astype(np.uint32)
+        assert np.array_equal(out, x[np.argsort(img, kind="stable")])
