@@ -18,6 +18,7 @@ merged bytes, which are identical for every p and C.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -191,6 +192,12 @@ def _empty_vals(A: _Arr, n: int):
 # --------------------------------------------------------------------------
 # core.hpp: diagonal_search / partition / diagonal_of
 # --------------------------------------------------------------------------
+def _host_device() -> int:
+    """GPU used for host-array calls: MERGEPATH_DEVICE, else 0 (as the C++
+    drop-in, b200_backend.hpp)."""
+    return int(os.environ.get("MERGEPATH_DEVICE", "0"))
+
+
 def diagonal_of(n: int, p: int, i: int) -> int:
     """core.hpp:90-92"""
     return i * n // p
@@ -200,21 +207,23 @@ def _search(A: _Arr, B: _Arr, diags: list[int], counter: list | None):
     count = len(diags)
     if count == 0:
         return []
-    dev = torch.device("cuda", _device_index(A)) if A.device else torch.device("cuda", 0)
+    if not A.device:  # host arrays: the ABI stages them (mp_diagonal_search_host)
+        d_h = np.asarray(diags, dtype=np.uint64)
+        o_h = np.zeros(count, dtype=np.uint64)
+        c_h = C.c_uint64(0)
+        N.check(N.lib.mp_diagonal_search_host(A.kt, A.ptr, A.n, B.ptr, B.n, d_h.ctypes.data,
+                                              count, o_h.ctypes.data, C.byref(c_h),
+                                              _host_device()))
+        if counter is not None:
+            counter[0] += int(c_h.value)
+        return [PartitionPoint(int(o), d - int(o))
+                for o, d in zip(o_h, [min(x, A.n + B.n) for x in diags])]
+    dev = torch.device("cuda", _device_index(A))
     d_t = torch.tensor(diags, dtype=torch.int64, device=dev)
     o_t = torch.empty(count, dtype=torch.int64, device=dev)
     c_t = torch.zeros(1, dtype=torch.int64, device=dev)
-    if A.device:
-        aptr, bptr, keep = A.ptr, B.ptr, None
-    else:  # stage host inputs for the search kernel
-        ks = N.KEY_SIZES[A.kt]
-        keep = [torch.from_numpy(np.frombuffer(x.obj.tobytes(), dtype=np.uint8)).to(dev)
-                if x.n else torch.empty(16, dtype=torch.uint8, device=dev)
-                for x in (A, B)]
-        aptr, bptr = keep[0].data_ptr(), keep[1].data_ptr()
-        del ks
     stream = torch.cuda.current_stream(dev).cuda_stream
-    N.check(N.lib.mp_diagonal_search(A.kt, aptr, A.n, bptr, B.n, d_t.data_ptr(), count,
+    N.check(N.lib.mp_diagonal_search(A.kt, A.ptr, A.n, B.ptr, B.n, d_t.data_ptr(), count,
                                      o_t.data_ptr(), c_t.data_ptr(), stream))
     offs = o_t.cpu().tolist()
     if counter is not None:
@@ -263,7 +272,7 @@ def _merge(A: _Arr, B: _Arr, out, a_vals, b_vals, out_vals):
                                _stream_ptr(A)))
     else:
         N.check(N.lib.mp_merge_host(A.kt, A.ptr, vp(AV), A.n, B.ptr, vp(BV), B.n, O.ptr,
-                                    vp(OV), 0))
+                                    vp(OV), _host_device()))
 
 
 def _merge_stats(A, B, p, stats):
@@ -320,7 +329,7 @@ def _segment_plan(A: _Arr, B: _Arr, p: int, cache_elems: int):
         st = np.zeros(iters, dtype=np.uint64)
         pc, mc = C.c_uint64(0), C.c_uint64(0)
         N.check(N.lib.mp_segment_plan_host(A.kt, A.ptr, A.n, B.ptr, B.n, p, cache_elems,
-                                           st.ctypes.data, None, C.byref(pc), C.byref(mc), 0))
+                                           st.ctypes.data, None, C.byref(pc), C.byref(mc), _host_device()))
         sa = st.tolist()
         plan_cmp, merge_cmp = pc.value, mc.value
     starts = [PartitionPoint(int(x), k * L - int(x)) for k, x in enumerate(sa)]
@@ -384,7 +393,7 @@ def _checksum(A: _Arr, B: _Arr) -> int:
                                         _stream_ptr(A)))
         return int(s.item()) & 0xFFFFFFFFFFFFFFFF
     s = C.c_uint64(0)
-    N.check(N.lib.mp_merge_checksum_host(A.kt, A.ptr, A.n, B.ptr, B.n, C.byref(s), 0))
+    N.check(N.lib.mp_merge_checksum_host(A.kt, A.ptr, A.n, B.ptr, B.n, C.byref(s), _host_device()))
     return s.value
 
 
@@ -446,7 +455,7 @@ def _sort(data, vals, key_type):
         O = _Arr(out, D.kt)
         N.check(N.lib.mp_sort_host(D.kt, D.ptr, V.ptr if V is not None else None, D.n,
                                    O.ptr, _Arr(out_vals, values=True).ptr if V is not None else None,
-                                   0))
+                                   _host_device()))
     return (out, out_vals) if out_vals is not None else out
 
 
