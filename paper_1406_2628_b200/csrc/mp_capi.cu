@@ -473,10 +473,6 @@ struct SortLayout {
 };
 // grid spacing of the fused two-round pass (mp_quad.cuh): the bare block
 // sort's run, so G divides every pair width 2w
-#ifndef MP_QUAD_DIV
-#define MP_QUAD_DIV 1  // G = 4352 / DIV (2176 measured slower: 3.71 ms)
-#endif
-constexpr uint32_t kQuadG = static_cast<uint32_t>(kBareRun) / MP_QUAD_DIV;
 
 template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
   using T = typename KT::T;
@@ -487,7 +483,8 @@ template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
   L.vals_off = up(n * sizeof(T));
   L.part_off = L.vals_off + (vals ? up(n * 4) : 0);
   L.quad_off = L.part_off + up((cdiv(n, NV) + 1) * sizeof(uint64_t));
-  L.total = L.quad_off + (!vals && sizeof(T) == 4 ? up((cdiv(n, kQuadG) + 4) * sizeof(QuadPt)) : 0);
+  L.total = L.quad_off +
+            (!vals && sizeof(T) == 4 ? up((2 * cdiv(n, 4096) + 32) * sizeof(QuadPt)) : 0);
   return L;
 }
 
@@ -607,15 +604,16 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   for (uint64_t w = run0; w < n; w *= 2)
     ++rounds;
   // MP_SORT_QUAD=1: fuse round pairs into one HBM pass (mp_quad.cuh).
-  // Opt-in: bit-exact, but measured on B200 (2^30 u32) at 3.48 ms (K5q) +
-  // 0.18 ms (K4q) per fused pass vs 2 x (1.25 + 0.11) ms for two plain
-  // rounds -- segments hold 0..2G outputs, so a CTA sized for 2G is half
-  // idle and 5 CTAs/SM cannot hide the serial-merge and load latencies.
+  // Opt-in: bit-exact, but measured on B200 (2^30 u32, per fused pass):
+  // K4q 0.18 + K4r 0.43 + K5e 2.41 = 3.0 ms vs 2 x (1.25 + 0.10) ms for two
+  // plain rounds -- K5e halves the HBM bytes but issues 57 instructions per
+  // element (two searches + two serial merges), so it is issue-bound above
+  // the time of the two HBM-bound rounds it replaces.
   static const bool quad_env = [] {
     const char *e = std::getenv("MP_SORT_QUAD");
     return e && std::strcmp(e, "1") == 0;
   }();
-  const bool use_quad = use_bare && quad_env;
+  const bool use_quad = (use_bare || use_warp) && quad_env;
   const int quad_passes = use_quad ? rounds / 2 : 0;
   const int passes = rounds - quad_passes;  // ping-pong swaps after the block sort
   // Block sort lands where an even/odd number of ping-pong passes ends in
@@ -682,10 +680,11 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   const uint32_t NV = sort_round_tile<KT, VALS>();
   uint64_t w = run0;
   if constexpr (kBare4) {
+    // fused round pairs (mp_quad.cuh v2): K4q crossings at grid G = NV,
+    // K4r exact 4-way splits at every NV-output tile, K5e tile merges
     for (int fused_left = quad_passes; fused_left > 0 && w < n; --fused_left, w *= 4) {
-      // rounds (w, 2w) in one pass: K4q crossings + K5q segment merges
       QuadPt *QP = reinterpret_cast<QuadPt *>(ws + L.quad_off);
-      const uint32_t G = static_cast<uint32_t>(kQuadG);
+      const uint32_t G = NV;
       const uint32_t lshift = static_cast<uint32_t>(__builtin_ctzll(4 * w / G));
       const uint64_t full = n / (4 * w);
       uint64_t lines = full << lshift;
@@ -698,16 +697,28 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
         }
         lines += cdiv(l[0] + l[1], G) + cdiv(l[2] + l[3], G);
       }
-      quad_partition_kernel<KT, kQuadG><<<static_cast<unsigned>(cdiv(lines, 128)), 128, 0, s>>>(
-          src, n, w, lshift, lines, QP);
-      MP_LAUNCHED("quad_partition_kernel");
-      constexpr int QNT = 2 * NT / MP_QUAD_DIV, QVT = VT;
-      static_assert(QNT / 2 * QVT >= int(kQuadG), "inner merges fit half a CTA");
-      constexpr uint32_t qsmem = merge_smem_bytes<KT, false, QNT, QVT>();
-      auto qkern = quad_merge_kernel<KT, QNT, QVT, kQuadG>;
+      const uint64_t qtiles = cdiv(n, NV);
+      QuadPt *QQ = QP + cdiv(n, G) + 8;
+      auto launch = [&](auto g_tag) -> int {
+        constexpr uint32_t GG = decltype(g_tag)::value;
+        quad_partition_kernel<KT, GG><<<static_cast<unsigned>(cdiv(lines, 128)), 128, 0, s>>>(
+            src, n, w, lshift, lines, QP);
+        MP_LAUNCHED("quad_partition_kernel");
+        quad_refine_kernel<KT, GG><<<static_cast<unsigned>(cdiv(qtiles, 128)), 128, 0, s>>>(
+            src, n, w, lshift, NV, qtiles, QP, QQ);
+        MP_LAUNCHED("quad_refine_kernel");
+        return MP_OK;
+      };
+      int rc = NV == kBareRun ? launch(std::integral_constant<uint32_t, uint32_t(kBareRun)>{})
+                              : launch(std::integral_constant<uint32_t, 4096u>{});
+      if (rc)
+        return rc;
+      static_assert(NT * VT >= 4352 + 2 * VT, "K5e: a tile's two inner merges fit the CTA");
+      constexpr uint32_t qsmem = merge_smem_bytes<KT, false, NT, VT>();
+      auto qkern = quad_tile_kernel<KT, NT, VT>;
       MP_CUDA(set_smem(qkern, qsmem));
-      qkern<<<static_cast<unsigned>(lines), QNT, qsmem, s>>>(src, dst, n, w, lshift, QP);
-      MP_LAUNCHED("quad_merge_kernel");
+      qkern<<<static_cast<unsigned>(qtiles), NT, qsmem, s>>>(src, dst, n, w, NV, QQ);
+      MP_LAUNCHED("quad_tile_kernel");
       std::swap(src, dst);
     }
   }

@@ -17,12 +17,15 @@
 //   crossing is thus a 4-way split (i0, i1, i2, i3) of the group.  The
 //   crossing at x = kG is preceded by ceil(y/G) y-crossings and vice versa,
 //   which gives every crossing its slot in path order directly.
-// K5q (quad_merge_kernel): one CTA per segment between consecutive
-//   crossings.  No grid line lies strictly inside a segment, so it holds at
-//   most G elements of X and G of Y: <= 2G outputs.  The CTA bulk-copies its four run slices
-//   into smem, merges R0/R1 (threads of the first half) and R2/R3 (second
-//   half) into registers, writes X and Y back over the windows, merges X
-//   with Y (all threads) and bulk-stores the segment.
+//   No grid line lies strictly inside a segment between consecutive
+//   crossings, so a segment holds at most G elements of X and G of Y.
+// K4r (quad_refine_kernel): the exact 4-way split at every tile boundary
+//   t*T: find the segment holding it, then a nested Merge Path search inside
+//   the segment (outer on X/Y, inner on R0/R1 and R2/R3 for X[x], Y[y]).
+// K5e (quad_tile_kernel): one CTA per tile of exactly T outputs bulk-copies
+//   its four run slices into smem, merges R0/R1 and R2/R3 (threads dealt to
+//   X and Y by size), writes X and Y back over the windows, merges X with Y
+//   and bulk-stores the tile.
 // Both inner merges and the outer one use take_b (ties to the left
 // operand), so the result is the two-round result byte for byte.
 #pragma once
@@ -140,24 +143,171 @@ __global__ void quad_partition_kernel(const typename KT::T *__restrict__ src,
   dst[1] = make_ulonglong2(pt.i[2], pt.i[3]);
 }
 
-// K5q: one CTA per segment.  NT threads, VT outputs each in the outer merge;
-// each half of the CTA covers one inner merge (NT/2 * VT >= G).
-template <class KT, int NT, int VT, uint32_t G>
-__global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
-    quad_merge_kernel(const typename KT::T *__restrict__ src,
-                      typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
-                      uint32_t lshift, const QuadPt *__restrict__ P) {
-  using T = typename KT::T;
-  constexpr uint32_t KS = sizeof(T);
-  constexpr int HALF = NT / 2;
+// ---------------------------------------------------------------------------
+// K4r / K5e (see the header).  An earlier variant ran one CTA per segment
+// (0..2G outputs, bimodal around G): half of every CTA idle, 3.48 ms per
+// fused pass.
+// ---------------------------------------------------------------------------
+
+// element x of merge(R0[0..l0), R1[0..l1)) (ties to R0) and its split
+template <class KT>
+__device__ __forceinline__ typename KT::T merged_at(const typename KT::T *R0, uint64_t l0,
+                                                    const typename KT::T *R1, uint64_t l1,
+                                                    uint64_t x) {
+  uint64_t lo = x > l1 ? x - l1 : 0, hi = x < l0 ? x : l0;
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (take_b<KT>(R1[x - 1 - mid], R0[mid]))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  const uint64_t b = x - lo;
+  const bool from_b = b < l1 && (lo >= l0 || take_b<KT>(R1[b], R0[lo]));
+  return from_b ? R1[b] : R0[lo];
+}
+
+// split of merge(R0, R1) at diagonal x, searched within [lo0, hi0]
+template <class KT>
+__device__ __forceinline__ uint64_t split_in(const typename KT::T *R0, uint64_t l0,
+                                             const typename KT::T *R1, uint64_t l1,
+                                             uint64_t x, uint64_t lo0, uint64_t hi0) {
+  uint64_t lo = x > l1 ? x - l1 : 0, hi = x < l0 ? x : l0;
+  lo = lo > lo0 ? lo : lo0;
+  hi = hi < hi0 ? hi : hi0;
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (take_b<KT>(R1[x - 1 - mid], R0[mid]))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+template <class KT>
+__device__ __forceinline__ typename KT::T elem_at_split(const typename KT::T *R0, uint64_t l0,
+                                                        const typename KT::T *R1, uint64_t l1,
+                                                        uint64_t x, uint64_t a) {
+  const uint64_t b = x - a;
+  const bool from_b = b < l1 && (a >= l0 || take_b<KT>(R1[b], R0[a]));
+  return from_b ? R1[b] : R0[a];
+}
+
+template <class KT>
+__device__ __forceinline__ uint64_t split_at(const typename KT::T *R0, uint64_t l0,
+                                             const typename KT::T *R1, uint64_t l1,
+                                             uint64_t x) {
+  uint64_t lo = x > l1 ? x - l1 : 0, hi = x < l0 ? x : l0;
+  while (lo < hi) {
+    const uint64_t mid = lo + ((hi - lo) >> 1);
+    if (take_b<KT>(R1[x - 1 - mid], R0[mid]))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+// K4r: Q[t] = the 4-way split at output position t*T of the fused pass (T
+// divides the group size 4w, so tiles never straddle groups).
+template <class KT, uint32_t G>
+__global__ void quad_refine_kernel(const typename KT::T *__restrict__ src, uint64_t n,
+                                   uint64_t w, uint32_t lshift, uint32_t T,
+                                   uint64_t tiles, const QuadPt *__restrict__ P,
+                                   QuadPt *__restrict__ Q) {
+  using T_ = typename KT::T;
+  const uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (t >= tiles)
+    return;
+  const uint64_t pos = t * T;
+  const uint64_t g = pos / (4 * w);
+  const uint64_t dl = pos - g * 4 * w;  // group-local output position
+  QuadPt out;
+  if (dl == 0) {
+    out.i[0] = out.i[1] = out.i[2] = out.i[3] = 0;
+  } else {
+    const QuadGroup q = quad_group(g, n, w);
+    const T_ *R0 = src + q.S, *R1 = R0 + w, *R2 = R1 + w, *R3 = R2 + w;
+    const uint64_t pts = q.S + 4 * w <= n
+                             ? (uint64_t(1) << lshift)
+                             : cdiv_dev(q.l[0] + q.l[1], G) + cdiv_dev(q.l[2] + q.l[3], G);
+    const QuadPt *Pg = P + (g << lshift);
+    auto diag = [&](uint64_t k) {
+      const QuadPt &p = Pg[k];
+      return p.i[0] + p.i[1] + p.i[2] + p.i[3];
+    };
+    // last crossing at or before dl (crossing 0 is at diagonal 0)
+    uint64_t lo = 0, hi = pts - 1;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) >> 1;
+      if (diag(mid) <= dl)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const QuadPt p0 = Pg[lo];
+    QuadPt p1;
+    if (lo + 1 < pts) {
+      p1 = Pg[lo + 1];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        p1.i[r] = q.l[r];
+    }
+    // segment: X-part = merge(R0[p0.i0..p1.i0), R1[..)), Y-part likewise
+    const T_ *A0 = R0 + p0.i[0], *A1 = R1 + p0.i[1], *B0 = R2 + p0.i[2], *B1 = R3 + p0.i[3];
+    const uint64_t la0 = p1.i[0] - p0.i[0], la1 = p1.i[1] - p0.i[1];
+    const uint64_t lb0 = p1.i[2] - p0.i[2], lb1 = p1.i[3] - p0.i[3];
+    const uint64_t nx = la0 + la1, ny = lb0 + lb1;
+    const uint64_t d = dl - (p0.i[0] + p0.i[1] + p0.i[2] + p0.i[3]);
+    // outer Merge Path search on (X-part, Y-part) at diagonal d, ties to X.
+    // The inner splits are monotone (a(x) non-decreasing in x, c(y) in y),
+    // so every probe narrows the range the next inner searches scan.
+    uint64_t xl = d > ny ? d - ny : 0, xh = d < nx ? d : nx;
+    uint64_t aL = 0, aH = la0, cL = 0, cH = lb0;  // a(x) for x in [xl,xh]; c(y)
+    while (xl < xh) {
+      const uint64_t x = xl + ((xh - xl) >> 1), y = d - 1 - x;
+      const uint64_t ax = split_in<KT>(A0, la0, A1, la1, x, aL, aH);
+      const uint64_t cy = split_in<KT>(B0, lb0, B1, lb1, y, cL, cH);
+      const T_ xv = elem_at_split<KT>(A0, la0, A1, la1, x, ax);
+      const T_ yv = elem_at_split<KT>(B0, lb0, B1, lb1, y, cy);
+      if (take_b<KT>(yv, xv)) {
+        xh = x;  // answer <= x: a(answer) <= a(x), y grows: c >= c(y)
+        aH = ax;
+        cL = cy;
+      } else {
+        xl = x + 1;  // answer > x: a >= a(x), y(answer) <= d-2-x < y: c <= c(y)
+        aL = ax;
+        cH = cy + 1 < lb0 ? cy + 1 : lb0;
+      }
+    }
+    const uint64_t x = xl, y = d - xl;
+    const uint64_t a = split_in<KT>(A0, la0, A1, la1, x, aL, aH);
+    const uint64_t c = split_in<KT>(B0, lb0, B1, lb1, y, cL, cH);
+    out.i[0] = p0.i[0] + a;
+    out.i[1] = p0.i[1] + (x - a);
+    out.i[2] = p0.i[2] + c;
+    out.i[3] = p0.i[3] + (y - c);
+  }
+  ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(Q + t);
+  dst[0] = make_ulonglong2(out.i[0], out.i[1]);
+  dst[1] = make_ulonglong2(out.i[2], out.i[3]);
+}
+
+// K5e: one CTA per tile of T outputs (NT*VT >= T + 2*VT).  Phase 1 deals
+// ceil(nx/VT) threads to X = merge(R0w, R1w) and the rest to Y; both are
+// written over their input windows; phase 2 merges X with Y.
+template <class KT, int NT, int VT>
+__global__ void __launch_bounds__(NT, 1536 / NT)
+    quad_tile_kernel(const typename KT::T *__restrict__ src,
+                     typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
+                     uint32_t T, const QuadPt *__restrict__ Q) {
+  using T_ = typename KT::T;
+  constexpr uint32_t KS = sizeof(T_);
   extern __shared__ __align__(128) char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
   const int tid = threadIdx.x;
-
-  // ---- setup by warp 0 only: the segment's crossings, four run slices and
-  //      their smem windows go to a header; lane 0 issues the bulk copies and
-  //      lanes 8r..8r+7 load window r's unaligned head/tail (< 16 B each) ----
-  static_assert(KS <= 8 || KS == 16, "edge lanes per window");
   struct Hdr {
     uint32_t oW[4];
     int cnt[4];
@@ -166,18 +316,15 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
   Hdr *hdr = reinterpret_cast<Hdr *>(smem + 16);
   constexpr uint32_t kWin0 = 64;
   if (tid < 32) {
-    const uint64_t b = blockIdx.x;
-    const uint64_t g = b >> lshift;
-    const uint64_t m = b & ((uint64_t(1) << lshift) - 1);
+    const uint64_t t = blockIdx.x;
+    const uint64_t pos = t * T;
+    const uint64_t g = pos / (4 * w);
     const QuadGroup q = quad_group(g, n, w);
-    // crossings in this group: 4w/G for a whole group, fewer for the last
-    const uint64_t pts = q.S + 4 * w <= n
-                             ? (uint64_t(1) << lshift)
-                             : cdiv_dev(q.l[0] + q.l[1], G) + cdiv_dev(q.l[2] + q.l[3], G);
-    const QuadPt p0 = P[(g << lshift) + m];
+    const QuadPt p0 = Q[t];
     QuadPt p1;
-    if (m + 1 < pts) {
-      p1 = P[(g << lshift) + m + 1];
+    const uint64_t gend = q.S + q.l[0] + q.l[1] + q.l[2] + q.l[3];
+    if (pos + T < gend) {
+      p1 = Q[t + 1];
     } else {
 #pragma unroll
       for (int r = 0; r < 4; ++r)
@@ -201,7 +348,7 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
         hdr->oW[r] = oW[r];
         hdr->cnt[r] = cnt[r];
       }
-      hdr->o0 = q.S + p0.i[0] + p0.i[1] + p0.i[2] + p0.i[3];
+      hdr->o0 = pos;
       mbar_init(bar, 1);
       fence_mbar_init();
       uint32_t lo[4], ib[4], tx = 0;
@@ -233,21 +380,22 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
   const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
   mbar_wait(bar, 0);
 
-  // ---- phase 1: X = merge(R0, R1) by threads [0, HALF), Y = merge(R2, R3)
-  //      by threads [HALF, NT), VT outputs each into registers ----
-  T keys[VT];
+  // ---- phase 1: dynamic split of the threads between X and Y ----
+  T_ keys[VT];
   uint32_t vals[VT];
-  const int side = tid >= HALF ? 1 : 0;
-  const int t1 = tid - side * HALF;
+  const int tx = (nx + VT - 1) / VT;
+  const int side = tid >= tx ? 1 : 0;
+  const int t1 = tid - side * tx;
   const uint32_t oA = side ? oW[2] : oW[0], oB = side ? oW[3] : oW[1];
   const int na = side ? cnt[2] : cnt[0], nb = side ? cnt[3] : cnt[1];
   const int d1 = t1 * VT;
-  if (d1 < na + nb) {
+  const bool act1 = d1 < na + nb;
+  if (act1) {
     int lo = d1 > nb ? d1 - nb : 0;
     int hi = d1 < na ? d1 : na;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (take_b<KT>(lds<T>(smem, oB + (d1 - 1 - mid) * KS), lds<T>(smem, oA + mid * KS)))
+      if (take_b<KT>(lds<T_>(smem, oB + (d1 - 1 - mid) * KS), lds<T_>(smem, oA + mid * KS)))
         hi = mid;
       else
         lo = mid + 1;
@@ -255,22 +403,21 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
     serial_merge<KT, VT, false>(smem, oA, na, oB, nb, 0, 0, lo, d1 - lo, keys, vals);
   }
   __syncthreads();  // every window consumed
-  // X at [oX, oX + nx), Y right behind it (reads past X's end land in Y or
-  // the slack and are never used)
-  constexpr uint32_t oX = 16;
-  const uint32_t oY = oX + nx * KS;
-  {
+  // X over [oW0, oW0 + nx), Y over [oW2, oW2 + ny): each fits in the span
+  // of the two windows it was merged from
+  const uint32_t oX = oW[0], oY = oW[2];
+  if (act1) {
     const uint32_t op = side ? oY : oX;
     const int lim = side ? ny : nx;
     if (d1 + VT <= lim) {
 #pragma unroll
       for (int k = 0; k < VT; ++k)
-        *reinterpret_cast<T *>(smem + op + (d1 + k) * KS) = keys[k];
-    } else if (d1 < lim) {
+        *reinterpret_cast<T_ *>(smem + op + (d1 + k) * KS) = keys[k];
+    } else {
 #pragma unroll
       for (int k = 0; k < VT; ++k)
         if (d1 + k < lim)
-          *reinterpret_cast<T *>(smem + op + (d1 + k) * KS) = keys[k];
+          *reinterpret_cast<T_ *>(smem + op + (d1 + k) * KS) = keys[k];
     }
   }
   __syncthreads();
@@ -282,28 +429,26 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
     int hi = d2 < nx ? d2 : nx;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (take_b<KT>(lds<T>(smem, oY + (d2 - 1 - mid) * KS), lds<T>(smem, oX + mid * KS)))
+      if (take_b<KT>(lds<T_>(smem, oY + (d2 - 1 - mid) * KS), lds<T_>(smem, oX + mid * KS)))
         hi = mid;
       else
         lo = mid + 1;
     }
     serial_merge<KT, VT, false>(smem, oX, nx, oY, ny, 0, 0, lo, d2 - lo, keys, vals);
   }
-  __syncthreads();  // X and Y consumed; stage the segment
+  __syncthreads();  // X and Y consumed
 
-  // staging congruent (mod 16) to the output address: the 16 B-aligned
-  // interior leaves with one bulk store, the < 16 B head and tail by LSU
-  T *out = dst + o0;
+  T_ *out = dst + o0;
   const uint32_t oS = mirror_off(16, out);
   if (d2 + VT <= total) {
 #pragma unroll
     for (int k = 0; k < VT; ++k)
-      *reinterpret_cast<T *>(smem + oS + (d2 + k) * KS) = keys[k];
+      *reinterpret_cast<T_ *>(smem + oS + (d2 + k) * KS) = keys[k];
   } else if (d2 < total) {
 #pragma unroll
     for (int k = 0; k < VT; ++k)
       if (d2 + k < total)
-        *reinterpret_cast<T *>(smem + oS + (d2 + k) * KS) = keys[k];
+        *reinterpret_cast<T_ *>(smem + oS + (d2 + k) * KS) = keys[k];
   }
   fence_proxy_async_smem();
   __syncthreads();
@@ -314,7 +459,7 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
     bulk_s2g(reinterpret_cast<char *>(out) + lo, smem + oS + lo, ib);
     bulk_commit();
   }
-  if (tid >= 32 && tid < 64) {  // head [0, lo) and tail [lo + ib, total*KS)
+  if (tid >= 32 && tid < 64) {
     const uint32_t bytes = static_cast<uint32_t>(total) * KS;
     const uint32_t hi = ib ? lo + ib : bytes;
     const uint32_t hlo = ib ? lo : bytes;
@@ -322,7 +467,7 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, false, NT>()))
     const uint32_t l = tid - 32;
     if (l < nh + nt) {
       const uint32_t e = l < nh ? l : (hi / KS) + (l - nh);
-      out[e] = lds<T>(smem, oS + e * KS);
+      out[e] = lds<T_>(smem, oS + e * KS);
     }
   }
   if (tid == 0 && ib)
