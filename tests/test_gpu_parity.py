@@ -826,3 +826,52 @@ def test_host_sort_pipelined(cuda, S, n):
     else:
         img = np.where(x & 0x80000000, ~x, x | 0x80000000).astype(np.uint32)
         assert np.array_equal(out, x[np.argsort(img, kind="stable")])
+
+
+def test_concurrent_calls_from_threads(cuda, port):
+    """Merges and sorts issued concurrently from several host threads, each
+    on its own stream (the library's scratch pool, host pipeline and launch
+    counter are shared), including host-buffer calls; all bit-exact."""
+    import threading
+    torch = _torch()
+    from paper_1406_2628_b200 import _native as N
+    rng = np.random.default_rng(61)
+    cases = []
+    for k in range(6):
+        na, nb = int(rng.integers(1, 3_000_000)), int(rng.integers(1, 3_000_000))
+        a = np.sort(rng.integers(0, 1 << 20, na).astype(np.int32))
+        b = np.sort(rng.integers(0, 1 << 20, nb).astype(np.int32))
+        x = rng.integers(0, 1 << 32, 1_000_003, dtype=np.uint64).astype(np.uint32)
+        cases.append((a, b, x))
+    errors = []
+
+    def work(k):
+        try:
+            a, b, x = cases[k]
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+                out = torch.empty(len(a) + len(b), dtype=torch.int32, device="cuda")
+                for _ in range(3):
+                    N.check(N.lib.mp_merge(N.KEY_I32, da.data_ptr(), None, len(a), db.data_ptr(),
+                                           None, len(b), out.data_ptr(), None, st.cuda_stream))
+                dx = torch.from_numpy(x).cuda()
+                N.check(N.lib.mp_sort(N.KEY_U32, dx.data_ptr(), None, len(x), None, 0,
+                                      st.cuda_stream))
+                st.synchronize()
+                ho = np.empty(len(a) + len(b), dtype=np.int32)
+                N.check(N.lib.mp_merge_host(N.KEY_I32, a.ctypes.data, None, len(a),
+                                            b.ctypes.data, None, len(b), ho.ctypes.data, None, 0))
+                want = np.sort(np.concatenate([a, b]), kind="stable")
+                assert np.array_equal(out.cpu().numpy(), want), "device merge"
+                assert np.array_equal(ho, want), "host merge"
+                assert np.array_equal(dx.cpu().numpy(), np.sort(x)), "sort"
+        except Exception as e:  # pragma: no cover
+            errors.append((k, repr(e)))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(cases))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
