@@ -875,3 +875,56 @@ def test_concurrent_calls_from_threads(cuda, port):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+def _extreme_pool(S):
+    """Key values at the edges of each type's order."""
+    if S == "f32":
+        bits = [0x00000000, 0x80000000, 0x00000001, 0x80000001, 0x7F7FFFFF, 0xFF7FFFFF,
+                0x7F800000, 0xFF800000, 0x7FC00000, 0xFFC00000, 0x7FFFFFFF, 0xFFFFFFFF,
+                0x3F800000, 0xBF800000, 0x007FFFFF, 0x807FFFFF]
+        return np.array(bits, dtype=np.uint32)
+    dt = {"u32": np.uint32, "i32": np.int32, "u64": np.uint64, "i64": np.int64}[S]
+    info = np.iinfo(dt)
+    vals = [info.min, info.min + 1, info.max, info.max - 1, 0, 1]
+    if info.min < 0:
+        vals += [-1, -2]
+    if np.dtype(dt).itemsize == 4:
+        vals += [0x7FFFFFFF if info.min < 0 else 0x80000000]
+    else:
+        vals += [(1 << 62)]
+    return np.array(vals, dtype=dt)
+
+
+def _order_sorted(S, x):
+    if S == "f32":
+        u = x.view(np.uint32)
+        key = np.where(u & 0x80000000, ~u, u | 0x80000000)
+        return u[np.argsort(key, kind="stable")]
+    return np.sort(x, kind="stable")
+
+
+@pytest.mark.parametrize("S", ("u32", "i32", "f32", "u64", "i64"))
+def test_extreme_keys_merge_and_sort(cuda, port, S):
+    """Keys at the type's extremes (min/max, sign boundaries; f32 +-0, +-inf,
+    NaNs with payloads, denormals, FLT_MAX) drawn with heavy repetition,
+    merged and sorted through the device, bit-exact vs the oracle; plus
+    all-equal inputs at the maximum and the minimum key."""
+    from paper_1406_2628_b200 import mergepath as mp
+    rng = np.random.default_rng(71)
+    pool = _extreme_pool(S)
+    for n in (1, 7, 4095, 4097, 8193, 70_001):
+        a = _order_sorted(S, pool[rng.integers(0, len(pool), n)])
+        b = _order_sorted(S, pool[rng.integers(0, len(pool), n + 3)])
+        want, _, _, _ = port.merge(S, a, b)
+        got = mp.parallel_merge(to_dev(a, S, cuda), to_dev(b, S, cuda), 4, key_type=key_type(S))
+        assert same(from_dev(got, S), want), (S, n, "merge")
+        d = pool[rng.integers(0, len(pool), n)]
+        want_s, _, _ = port.merge_sort(S, d)
+        got_s = mp.parallel_merge_sort(to_dev(d, S, cuda), 4, key_type=key_type(S))
+        assert same(from_dev(got_s, S), want_s), (S, n, "sort")
+    for v in (pool.max() if S != "f32" else pool[-5], pool.min() if S != "f32" else pool[7]):
+        d = np.full(10_007, v, dtype=pool.dtype)
+        want_s, _, _ = port.merge_sort(S, d)
+        got_s = mp.parallel_merge_sort(to_dev(d, S, cuda), 4, key_type=key_type(S))
+        assert same(from_dev(got_s, S), want_s)
