@@ -503,6 +503,31 @@ int block_sort_engine() {
   return e;
 }
 
+// K3w's levels above the warp: bitonic stages through smem (default) or
+// Merge Path passes (MP_K3W=merge), see mp_bsort.cuh.
+bool k3w_cross_warp_bitonic() {
+  static const bool b = [] {
+    const char *v = std::getenv("MP_K3W");
+    return !(v && std::strcmp(v, "merge") == 0);
+  }();
+  return b;
+}
+
+// The 16-keys-per-thread block sort: K3w (default: warp bitonic levels +
+// Merge Path passes in smem) or K3t (MP_K3W=tr: the whole bitonic network
+// in registers with smem transposes), see mp_bsort.cuh.  Same runs, same
+// bytes.  B200 (2^30 u32, ncu): K3w 8.26 ms (5.9 G warp instructions, ALU
+// pipe 90.5 %), K3t 8.44 ms (5.8 G, ALU pipe 80.5 %, LSU 58.6 %) -- both
+// are bound by the ALU pipe's min/max rate (VIMNMX issues at half rate and a
+// compare-exchange whose direction depends on the lane costs two of them).
+bool k3w_transposed() {
+  static const bool b = [] {
+    const char *v = std::getenv("MP_K3W");
+    return v && std::strcmp(v, "tr") == 0;
+  }();
+  return b;
+}
+
 // Run length the block sort leaves and the round tile (mp_sort's schedule).
 template <class KT, bool VALS> uint64_t sort_run0() {
   constexpr bool bare4 = !VALS && sizeof(typename KT::T) == 4 && KT::kind != kElement;
@@ -627,21 +652,30 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   bool block_sorted = false;
   if constexpr (kBare4) {
     if (use_warp) {
-      constexpr uint32_t smem = warp_sort_smem_bytes<kWarpNT>();
       const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
       const uint64_t whole = al ? n / kWarpRun : 0, blocks = cdiv(n, kWarpRun);
-      if (whole) {
-        auto kern = block_sort_warp_kernel<KT, kWarpNT, true>;
-        MP_CUDA(set_smem(kern, smem));
-        kern<<<static_cast<unsigned>(whole), kWarpNT, smem, s>>>(in, src, n, 0);
-        MP_LAUNCHED("block_sort_warp_kernel");
-      }
-      if (blocks > whole) {
-        auto kern = block_sort_warp_kernel<KT, kWarpNT, false>;
-        MP_CUDA(set_smem(kern, smem));
-        kern<<<static_cast<unsigned>(blocks - whole), kWarpNT, smem, s>>>(in, src, n, whole);
-        MP_LAUNCHED("block_sort_warp_kernel(tail)");
-      }
+      auto launch = [&](auto kaligned, auto kunaligned, uint32_t smem) -> int {
+        if (whole) {
+          MP_CUDA(set_smem(kaligned, smem));
+          kaligned<<<static_cast<unsigned>(whole), kWarpNT, smem, s>>>(in, src, n, 0);
+          MP_LAUNCHED("block_sort_warp_kernel");
+        }
+        if (blocks > whole) {
+          MP_CUDA(set_smem(kunaligned, smem));
+          kunaligned<<<static_cast<unsigned>(blocks - whole), kWarpNT, smem, s>>>(in, src, n, whole);
+          MP_LAUNCHED("block_sort_warp_kernel(tail)");
+        }
+        return MP_OK;
+      };
+      const int rc = k3w_transposed()
+                         ? launch(block_sort_tr_kernel<KT, kWarpNT, true>,
+                                  block_sort_tr_kernel<KT, kWarpNT, false>,
+                                  tr_sort_smem_bytes<kWarpNT>())
+                         : launch(block_sort_warp_kernel<KT, kWarpNT, true>,
+                                  block_sort_warp_kernel<KT, kWarpNT, false>,
+                                  warp_sort_smem_bytes<kWarpNT>());
+      if (rc)
+        return rc;
       block_sorted = true;
     } else if (use_bare) {
       constexpr uint32_t smem = bare_sort_smem_bytes<kBareNT, kBareVT>();

@@ -611,12 +611,15 @@ print("FUSED OK")
 
 
 @pytest.mark.parametrize("S", ("u32", "i32", "f32"))
-@pytest.mark.parametrize("engine,quad", [("warp", "0"), ("bare", "0"), ("bare", "1")])
-def test_fused_round_sorts_vs_oracle(cuda, S, engine, quad):
+@pytest.mark.parametrize("engine,quad,k3w", [("warp", "0", "merge"), ("warp", "0", "tr"),
+                                             ("warp", "1", "merge"), ("bare", "0", ""),
+                                             ("bare", "1", "")])
+def test_fused_round_sorts_vs_oracle(cuda, S, engine, quad, k3w):
     """Bare 32-bit sorts through each block sort -- K3w (default, 8192-key
-    runs, warp-level bitonic levels) and K3b (4352-key runs) -- then plain
-    rounds or, after K3b, fused two-round passes (MP_SORT_QUAD=1,
-    mp_quad.cuh).  The switches are read once per process, hence the
+    runs, warp bitonic levels + Merge Path passes), K3t (MP_K3W=tr: the
+    bitonic network in registers with smem transposes, same runs) and K3b
+    (4352-key runs) -- then plain rounds or fused two-round passes
+    (MP_SORT_QUAD=1, mp_quad.cuh).  The switches are read once per process, hence the
     subprocess."""
     import os
     import subprocess
@@ -625,7 +628,7 @@ def test_fused_round_sorts_vs_oracle(cuda, S, engine, quad):
     root = str(Path(__file__).resolve().parents[1])
     r = subprocess.run([sys.executable, "-c", _FUSED_SORT_CHECK, root, S], capture_output=True,
                        text=True, timeout=900,
-                       env=dict(os.environ, MP_SORT_QUAD=quad, MP_BLOCK_SORT=engine))
+                       env=dict(os.environ, MP_SORT_QUAD=quad, MP_BLOCK_SORT=engine, MP_K3W=k3w))
     assert r.returncode == 0 and "FUSED OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
 
 
