@@ -169,6 +169,8 @@ constexpr uint64_t kBareRun = kBareNT * kBareVT;
 #endif                  // one more smem pass; B200 2^30 u32 31.52 -> 31.36 ms
 constexpr int kWarpNT = MP_WARP_NT;
 constexpr uint64_t kWarpRun = kWarpNT * 16;
+constexpr uint32_t kBigTile4 = 8192;  // round tile after K3w (sort_round_tile)
+constexpr int kBigTileNT = 384;       // 384 x 23 >= 8192
 
 template <class K> cudaError_t set_smem(K kernel, uint32_t bytes) {
   if (bytes <= 48 * 1024)
@@ -537,22 +539,48 @@ template <class KT, bool VALS> uint64_t sort_run0() {
     return kWarpRun;
   return kRun;
 }
+bool sort_quad_env() {
+  static const bool b = [] {
+    const char *e = std::getenv("MP_SORT_QUAD");
+    return e && std::strcmp(e, "1") == 0;
+  }();
+  return b;
+}
+// Round tile after K3w's 8192-key runs: kBigTile4 (8192 = 384 threads x 23
+// outputs: half the K4 split searches of 4096-output tiles) unless
+// MP_SORT_TILE=4096 or the fused two-round pass (grid G = tile) is on.
+bool sort_big_tile_env() {
+  static const bool b = [] {
+    const char *e = std::getenv("MP_SORT_TILE");
+    return !(e && std::atoi(e) == 4096);
+  }();
+  return b;
+}
 template <class KT, bool VALS> uint32_t sort_round_tile() {
-  return sort_run0<KT, VALS>() == kBareRun ? static_cast<uint32_t>(kBareRun)
-                                           : SortMergeCfg<KT>::TILE;
+  const uint64_t r0 = sort_run0<KT, VALS>();
+  if (r0 == kBareRun)
+    return static_cast<uint32_t>(kBareRun);
+  if (sizeof(typename KT::T) == 4 && !VALS && KT::kind != kElement && r0 % kBigTile4 == 0 &&
+      sort_big_tile_env() && !sort_quad_env())
+    return kBigTile4;
+  return SortMergeCfg<KT>::TILE;
 }
 
 // Plain bottom-up rounds over sorted runs of width w0 held in `src`
 // (sort.hpp:71-128): per round K4 (pair-local split points at tile NV) and
 // K2 over RoundMap, ping-pong src <-> dst.  *res / *resv receive the buffer
 // holding the result.
-template <class KT, bool VALS>
+template <class KT, bool VALS, int NT = SortMergeCfg<KT>::NT, int VT = SortMergeCfg<KT>::VT>
 int sort_rounds_from(typename KT::T *src, uint32_t *srcv, typename KT::T *dst,
                      uint32_t *dstv, uint64_t n, uint64_t w0, uint32_t NV,
                      uint64_t *P, cudaStream_t s, typename KT::T **res,
                      uint32_t **resv) {
   using T = typename KT::T;
-  constexpr int NT = SortMergeCfg<KT>::NT, VT = SortMergeCfg<KT>::VT;
+  if constexpr (sizeof(T) == 4 && !VALS && NT == SortMergeCfg<KT>::NT) {
+    if (NV > static_cast<uint32_t>(NT * VT))  // kBigTile4 rounds after K3w
+      return sort_rounds_from<KT, VALS, kBigTileNT, VT>(src, srcv, dst, dstv, n, w0, NV, P, s,
+                                                        res, resv);
+  }
   const uint64_t tiles = cdiv(n, NV);
   constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
   auto kern = merge_tiles_kernel<KT, VALS, NT, VT, RoundMap, false>;
@@ -634,11 +662,7 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   // plain rounds -- K5e halves the HBM bytes but issues 57 instructions per
   // element (two searches + two serial merges), so it is issue-bound above
   // the time of the two HBM-bound rounds it replaces.
-  static const bool quad_env = [] {
-    const char *e = std::getenv("MP_SORT_QUAD");
-    return e && std::strcmp(e, "1") == 0;
-  }();
-  const bool use_quad = (use_bare || use_warp) && quad_env;
+  const bool use_quad = (use_bare || use_warp) && sort_quad_env();
   const int quad_passes = use_quad ? rounds / 2 : 0;
   const int passes = rounds - quad_passes;  // ping-pong swaps after the block sort
   // Block sort lands where an even/odd number of ping-pong passes ends in
