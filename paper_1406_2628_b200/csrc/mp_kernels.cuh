@@ -291,13 +291,22 @@ __host__ __device__ constexpr int stage_elems() {
   return (VT & 1) ? NT * VT : NT * VT + (NT * VT) / 32;
 }
 
+// Bare keys (no values, not the AoS element) run K2 with sentinels: VT
+// copies of the largest key after A's window and one after B's, so every
+// thread takes the bounds-free serial merge (serial_merge, SENT = true).
+template <class KT, bool VALS>
+__host__ __device__ constexpr bool merge_sentinels() {
+  return !VALS && KT::kind != kElement;
+}
+
 template <class KT, bool VALS, int NT, int VT>
 __host__ __device__ constexpr uint32_t merge_smem_bytes() {
   using T = typename KT::T;
   constexpr uint32_t NV = NT * VT;
   constexpr uint32_t in_bytes =
       // windows + alignment gaps + one element of read slack per window
-      NV * sizeof(T) + 96 + (VALS ? NV * 4 + 64 : 0);
+      NV * sizeof(T) + 96 + (VALS ? NV * 4 + 64 : 0) +
+      (merge_sentinels<KT, VALS>() ? (VT + 1) * sizeof(T) + 16 : 0);
   constexpr uint32_t st_bytes =
       stage_elems<NT, VT>() * sizeof(T) + 16 +
       (VALS ? stage_elems<NT, VT>() * 4 + 16 : 0);
@@ -382,7 +391,13 @@ __device__ __forceinline__ T lds(const char *smem, uint32_t off) {
 // window's end) the bounds tests vanish and the cursors are byte offsets
 // (~8 instructions per output).  Loads may touch one element past a window
 // (into the next window or the slack) and are then never used.
-template <class KT, int VT, bool VALS>
+// SENT (bare keys, sentinels behind both windows -- see merge_sentinels):
+// every thread takes the fast path.  Once A is exhausted its cursor walks
+// A's VT sentinels (the largest key), which lose to every smaller B key and
+// tie with a B key equal to them -- emitting the same value -- and B's
+// cursor never passes its own sentinel (never strictly below an A key), so
+// the VT output values are exact; outputs past the window are not stored.
+template <class KT, int VT, bool VALS, bool SENT = false>
 __device__ __forceinline__ void serial_merge(const char *smem, uint32_t oA,
                                              int na, uint32_t oB, int nb,
                                              uint32_t oAv, uint32_t oBv, int i,
@@ -392,7 +407,8 @@ __device__ __forceinline__ void serial_merge(const char *smem, uint32_t oA,
   constexpr uint32_t KS = sizeof(T);
   uint32_t pa = oA + i * KS, pb = oB + j * KS;
   uint32_t pva = oAv + i * 4u, pvb = oBv + j * 4u;
-  if (i + VT <= na && j + VT <= nb) {
+  static_assert(!(SENT && VALS), "sentinels are for bare keys");
+  if (SENT || (i + VT <= na && j + VT <= nb)) {
     T ka = lds<T>(smem, pa), kb = lds<T>(smem, pb);
 #pragma unroll
     for (int k = 0; k < VT; ++k) {
@@ -501,8 +517,9 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
   const char *gA = reinterpret_cast<const char *>(a + win.a0);
   const char *gB = reinterpret_cast<const char *>(b + win.b0);
   const uint32_t bA = na_t * KS, bB = nb_t * KS;
+  constexpr bool SENT = merge_sentinels<KT, VALS>();
   const uint32_t oA = mirror_off(16, gA);
-  const uint32_t oB = mirror_off(oA + bA, gB);
+  const uint32_t oB = mirror_off(oA + bA + (SENT ? VT * KS : 0), gB);
   const char *gAv = nullptr, *gBv = nullptr;
   uint32_t oAv = 0, oBv = 0;
   if constexpr (VALS) {
@@ -561,6 +578,11 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
       else if (w == 3)
         stage_edges<4>(smem, oBv, gBv, nb_t * 4, l);
     }
+    if constexpr (SENT) {
+      static_assert(VT < 32, "one sentinel per lane");
+      if (w == 2 && l <= VT)
+        *reinterpret_cast<T *>(smem + (l < VT ? oA + bA + l * KS : oB + bB)) = KT::max_key();
+    }
   }
   __syncthreads();
   if constexpr (!PEER)
@@ -586,8 +608,8 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
   //     (into the next window or the slack) but are never used. ---
   T keys[VT];
   uint32_t vals[VT];
-  serial_merge<KT, VT, VALS>(smem, oA, na_t, oB, nb_t, oAv, oBv, i, j, keys,
-                             vals);
+  serial_merge<KT, VT, VALS, SENT>(smem, oA, na_t, oB, nb_t, oAv, oBv, i, j, keys,
+                                   vals);
   if constexpr (SINK) {
     unsigned long long acc = 0;
 #pragma unroll
