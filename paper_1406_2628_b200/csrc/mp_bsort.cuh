@@ -214,9 +214,66 @@ __device__ __forceinline__ void ce_dir(uint32_t &x, uint32_t y, bool upper) {
 
 __host__ __device__ __forceinline__ constexpr int pad32(int p) { return p + (p >> 5); }
 
+// Pass layout: run r of width W at word r * (W + 32) (32-aligned, so
+// pad32(run + k) = pad32(run) + pad32(k) and a thread's 16 keys -- at a
+// multiple of 16 -- land at pad32(o) + q), followed by 16 copies of the
+// sentinel 0xFFFFFFFF: A's cursor may walk 16 of them, so it needs no
+// saturation (see the K3b header for why the output bytes stay exact).
 template <int NT>
 __host__ __device__ constexpr uint32_t warp_sort_smem_bytes() {
-  return static_cast<uint32_t>(pad32(NT * 16 + NT * 16 / 512 + 32)) * 4 + 64;
+  return static_cast<uint32_t>(pad32(NT * 16 + NT * 16 / 512 * 32 + 32)) * 4 + 64;
+}
+
+// Merge Path passes over runs of W, 2W, .. < NV (compile-time widths: the
+// run/pair/diagonal arithmetic is shifts and masks, the stores take
+// immediate offsets).  B200 ncu, 2^30 keys, before: 321 + ~150 (search)
+// warp instructions per pass and warp with runtime widths (an integer
+// division per pass), a saturating A cursor and per-key padded addresses.
+template <int W, int NV>
+__device__ __forceinline__ void warp_sort_passes(uint32_t (&x)[16], uint32_t *s, int p0) {
+  if constexpr (W < NV) {
+    constexpr int VT = 16, S = W + 32;
+    {
+      const int r = p0 / W, off = p0 % W;
+      uint32_t *p = s + pad32(r * S + off);
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        p[q] = x[q];
+      if (off + VT == W) {
+        uint32_t *ps = s + pad32(r * S + W);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          ps[q] = 0xFFFFFFFFu;
+      }
+    }
+    __syncthreads();
+    const int diag = p0 % (2 * W);
+    const int aO = (p0 / (2 * W)) * 2 * S;
+    const int bO = aO + S;
+    int lo = diag > W ? diag - W : 0;
+    int hi = diag < W ? diag : W;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s[pad32(bO + diag - 1 - mid)] < s[pad32(aO + mid)])
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    int pa = aO + lo, pb = bO + (diag - lo);
+    uint32_t ka = s[pad32(pa)], kb = s[pad32(pb)];
+#pragma unroll
+    for (int q = 0; q < VT; ++q) {
+      const bool tb = kb < ka;
+      x[q] = min(ka, kb);
+      pa += tb ? 0 : 1;
+      pb += tb ? 1 : 0;
+      const uint32_t nx = s[pad32(tb ? pb : pa)];
+      kb = tb ? nx : kb;
+      ka = tb ? ka : nx;
+    }
+    __syncthreads();
+    warp_sort_passes<2 * W, NV>(x, s, p0);
+  }
 }
 
 template <class KT, int NT, bool ALIGNED>
@@ -284,45 +341,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT)
 
   // ---- smem Merge Path passes: runs of 512 -> NV ----
   const int p0 = tid * VT;
-#pragma unroll 1
-  for (int w = 512; w < NV; w *= 2) {
-    {
-      const int r = p0 / w, off = p0 % w;
-      const int o = r * (w + 1) + off;
-#pragma unroll
-      for (int q = 0; q < VT; ++q)
-        s[pad32(o + q)] = x[q];
-      if (off + VT == w)
-        s[pad32(o + VT)] = 0xFFFFFFFFu;
-    }
-    __syncthreads();
-    const int diag = p0 % (2 * w);
-    const int aO = (p0 / (2 * w)) * 2 * (w + 1);
-    const int bO = aO + w + 1;
-    int lo = diag > w ? diag - w : 0;
-    int hi = diag < w ? diag : w;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (s[pad32(bO + diag - 1 - mid)] < s[pad32(aO + mid)])
-        hi = mid;
-      else
-        lo = mid + 1;
-    }
-    int pa = aO + lo, pb = bO + (diag - lo);
-    const int ea = aO + w;
-    uint32_t ka = s[pad32(pa)], kb = s[pad32(pb)];
-#pragma unroll
-    for (int q = 0; q < VT; ++q) {
-      const bool tb = kb < ka;
-      x[q] = tb ? kb : ka;
-      pa = tb ? pa : min(pa + 1, ea);
-      pb = tb ? pb + 1 : pb;
-      const uint32_t nx = s[pad32(tb ? pb : pa)];
-      kb = tb ? nx : kb;
-      ka = tb ? ka : nx;
-    }
-    __syncthreads();
-  }
+  warp_sort_passes<512, NV>(x, s, p0);
 
   // ---- x = sorted positions [p0, p0 + 16) of the block ----
   if constexpr (ALIGNED) {
