@@ -225,7 +225,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
                                                wsp.data_ptr(), stream.cuda_stream))
                 if evs is not None:
                     evs[1].record(stream)
-            launches_per_step = 2  # K1 + K2
+            launches_per_step = None  # K1 + K2 (K2 alone for a one-wave merge), measured
             units = n
         else:
             data0 = make_inputs(torch, N, cfg, dev, stream)
@@ -279,7 +279,9 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
 
     if cfg["kind"] == "merge":
         alg_bytes = n * cfg["bytes_per"]  # read A+B once, write S once
-        kname = "merge_tiles_kernel (K2); step = K1 grid-snapped split search + K2"
+        kname = ("merge_tiles_kernel (K2); step = K1 grid-snapped split search + K2"
+                 if launches_per_step > 1 else
+                 "merge_tiles_kernel with in-CTA split search (one-wave merge: one launch)")
     else:
         alg_bytes = n * 8 * (1 + sort_rounds(n))
         kname = "mp_sort: block_sort_warp + 17 x (round_partition + merge_tiles)"

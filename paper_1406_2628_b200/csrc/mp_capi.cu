@@ -212,13 +212,30 @@ template <class KT> uint64_t merge_ws_bytes(uint64_t n) {
   return (merge_tiles<KT>(n) + 1 + fine) * sizeof(uint64_t);
 }
 
-// K1 at tile spacing: P[t] = a_off on diagonal t*NV.
+// Merges of at most this many plan tiles run as ONE kernel: each K2 CTA
+// searches its own split points (SearchMap), no K1 launch.  One wave of
+// 512-thread CTAs at 4 per SM on 148 SMs; beyond it every extra wave would
+// pay the search latency again.  B200, config 1 (2^20 + 2^20 u32): see
+// DESIGN.md.  MP_MERGE_FUSE_TILES overrides (0 = always K1 + K2).
+uint64_t merge_fuse_tiles() {
+  static const uint64_t v = [] {
+    const char *e = std::getenv("MP_MERGE_FUSE_TILES");
+    return e ? static_cast<uint64_t>(std::atoll(e)) : uint64_t(592);
+  }();
+  return v;
+}
+template <class KT> bool merge_fused(uint64_t n) {
+  return cdiv(n, uint64_t(MergeCfg<KT>::NT) * MergeCfg<KT>::VT) <= merge_fuse_tiles();
+}
+
+// K1 at tile spacing: P[t] = a_off on diagonal t*NV.  (Nothing to do for a
+// fused small merge: merge_exec's CTAs search their own split points.)
 template <class KT>
 int merge_plan(const void *a, uint64_t na, const void *b, uint64_t nb,
                uint64_t *P, cudaStream_t s) {
   constexpr uint64_t NV = MergeCfg<KT>::NT * MergeCfg<KT>::VT;
   const uint64_t n = na + nb;
-  if (n == 0)
+  if (n == 0 || merge_fused<KT>(n))
     return MP_OK;
   if (merge_tiles<KT>(n) >= (1ull << 31))
     return fail(MP_ERR_INVALID, "merge too large (%llu elements)",
@@ -239,6 +256,16 @@ int merge_exec(const void *a, const uint32_t *av, uint64_t na, const void *b,
   if (n == 0)
     return MP_OK;
   const uint64_t tiles = cdiv(n, NV);
+  if (merge_fused<KT>(n)) {
+    constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
+    auto kern = merge_tiles_kernel<KT, VALS, NT, VT, SearchMap, SINK>;
+    MP_CUDA(set_smem(kern, smem));
+    kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
+        SearchMap{na, n, NV}, static_cast<const T *>(a), av, static_cast<const T *>(b), bv,
+        static_cast<T *>(out), outv, sum, 0);
+    MP_LAUNCHED("merge_tiles_kernel(search)");
+    return MP_OK;
+  }
   if constexpr (NT != MergeCfg<KT>::NT) {
     // the plan is at the wider tile: refine it to this tile's split points
     // (bounded searches between neighbouring planned points), stored behind
@@ -440,6 +467,16 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
   if (tiles >= (1ull << 31))
     return fail(MP_ERR_INVALID, "merge too large (%llu elements)",
                 (unsigned long long)n);
+  if (!PEER && merge_fused<KT>(n)) {  // one wave: CTAs search their own splits
+    constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
+    auto kern = merge_tiles_kernel<KT, VALS, NT, VT, SearchMap, SINK>;
+    MP_CUDA(set_smem(kern, smem));
+    kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
+        SearchMap{na, n, NV}, static_cast<const T *>(a), av, static_cast<const T *>(b), bv,
+        static_cast<T *>(out), outv, sum, 0);
+    MP_LAUNCHED("merge_tiles_kernel(search)");
+    return MP_OK;
+  }
   ScratchGuard P;
   if (int rc = alloc_scratch(P, merge_ws_bytes<KT>(n), s))
     return rc;
@@ -606,8 +643,15 @@ int sort_rounds_from(typename KT::T *src, uint32_t *srcv, typename KT::T *dst,
       MP_LAUNCHED("merge_tiles_kernel(round)");
       return MP_OK;
     };
-    if (int rc = run_overlapped(tiles, tiles, split, tile, s))
+    if (tiles <= merge_fuse_tiles()) {  // one wave: CTAs search their own splits
+      auto kfs = merge_tiles_kernel<KT, VALS, NT, VT, RoundSearchMap, false>;
+      MP_CUDA(set_smem(kfs, smem));
+      kfs<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
+          RoundSearchMap{n, w, NV, tshift}, src, srcv, src, srcv, dst, dstv, nullptr, 0);
+      MP_LAUNCHED("merge_tiles_kernel(round, search)");
+    } else if (int rc = run_overlapped(tiles, tiles, split, tile, s)) {
       return rc;
+    }
     std::swap(src, dst);
     std::swap(srcv, dstv);
   }

@@ -46,6 +46,36 @@ __device__ __forceinline__ uint64_t diag_search_global(
   return lo;
 }
 
+// The same split found by one warp with 32-ary steps: lane l probes
+// lo + l*step (step = ceil(span/32)); the predicate take_b(B[d-1-m], A[m])
+// is false..true along m (core.hpp:110), so the first lane that sees true
+// brackets the split between its probe and the previous lane's.  About
+// log32(span) + 1 dependent rounds of loads instead of log2(span): for a CTA
+// that searches its own tile boundary (SearchMap) the latency is what
+// counts.  All lanes return the same (exact) split.
+template <class KT>
+__device__ __forceinline__ uint64_t diag_search_warp(
+    const typename KT::T *__restrict__ a, uint64_t na,
+    const typename KT::T *__restrict__ b, uint64_t nb, uint64_t d, int lane) {
+  uint64_t lo = d > nb ? d - nb : 0;
+  uint64_t hi = d < na ? d : na;  // split in [lo, hi]
+  while (lo < hi) {
+    const uint64_t step = (hi - lo + 31) >> 5;
+    const uint64_t m = lo + static_cast<uint64_t>(lane) * step;
+    const bool t = m >= hi || take_b<KT>(b[d - 1 - m], a[m]);
+    const unsigned ball = __ballot_sync(0xffffffffu, t);
+    if (ball == 0) {  // every probe false: split above the last probe
+      lo = lo + 31 * step + 1;
+    } else {
+      const int k = __ffs(ball) - 1;  // first probe that is true
+      const uint64_t mk = lo + static_cast<uint64_t>(k) * step;
+      hi = mk < hi ? mk : hi;
+      lo = k ? lo + static_cast<uint64_t>(k - 1) * step + 1 : lo;
+    }
+  }
+  return lo;
+}
+
 // The same search with the top levels snapped to a shared grid (every
 // GRID-th element of A and B).  A probe at a grid position mid is decided
 // from the two grid neighbours of B[d-1-mid] when they bracket A[mid]
@@ -210,6 +240,39 @@ struct PlainMap {
   }
 };
 
+// Plain merge whose tile split points are searched by the tile's own CTA
+// (no K1 launch): for merges that fit in one wave of CTAs, where K1's launch
+// and dependent-probe latency is a large share of the call (config 1:
+// K1 ~15 us cold + K2 ~10 us).  Warp 0 searches diagonal t*NV and warp 1
+// diagonal (t+1)*NV (diag_search_warp: core.hpp:99-132 semantics, exact
+// split points), then window() takes them like PlainMap takes P[t], P[t+1].
+struct SearchMap {
+  uint64_t na, n;
+  uint32_t nv;
+  static constexpr bool kSearch = true;
+  // split point of boundary `end` (0: tile start, 1: tile end) of tile t
+  template <class KT>
+  __device__ __forceinline__ uint64_t split(const typename KT::T *a, const typename KT::T *b,
+                                            uint64_t t, int end, int lane) const {
+    const uint64_t d = (t + end) * nv < n ? (t + end) * nv : n;
+    return diag_search_warp<KT>(a, na, b, n - na, d, lane);
+  }
+  __device__ __forceinline__ TileWin window(uint64_t t, uint64_t a0, uint64_t a1) const {
+    const uint64_t d0 = t * nv;
+    const uint64_t d1 = d0 + nv < n ? d0 + nv : n;
+    TileWin w;
+    w.a0 = a0;
+    w.b0 = d0 - a0;
+    w.o0 = d0;
+    w.na = static_cast<int>(a1 - a0);
+    w.nb = static_cast<int>((d1 - a1) - (d0 - a0));
+    return w;
+  }
+};
+template <class Map, class = void> struct map_searches : std::false_type {};
+template <class Map>
+struct map_searches<Map, std::void_t<decltype(Map::kSearch)>> : std::true_type {};
+
 // One bottom-up round over runs of `width` (sort.hpp:71-101): pair k merges
 // A = src[2kw, 2kw+w) with B = src[2kw+w, 2kw+2w) (clipped to n); an
 // unpaired tail run has an empty B and is copied.  The tile NV divides the
@@ -238,6 +301,44 @@ struct RoundMap {
     const uint64_t dl1 = dl0 + nv < la + lb ? dl0 + nv : la + lb;
     const uint64_t a0 = P[t];
     const uint64_t a1 = (dl1 == la + lb) ? la : P[t + 1];
+    TileWin w;
+    w.a0 = s + a0;
+    w.b0 = s + la + (dl0 - a0);
+    w.o0 = d0;
+    w.na = static_cast<int>(a1 - a0);
+    w.nb = static_cast<int>((dl1 - a1) - (dl0 - a0));
+    return w;
+  }
+};
+
+// RoundMap whose split points the tile's CTA searches itself (SearchMap's
+// scheme for rounds of small sorts: one launch per round instead of K4 + K2).
+struct RoundSearchMap {
+  uint64_t n;
+  uint64_t width;
+  uint32_t nv;
+  uint32_t tshift;
+  static constexpr bool kSearch = true;
+  template <class KT>
+  __device__ __forceinline__ uint64_t split(const typename KT::T *src, const typename KT::T *,
+                                            uint64_t t, int end, int lane) const {
+    const uint64_t d0 = t * nv;
+    const uint64_t s = round_pair_start(t, nv, tshift);
+    const uint64_t la = (n - s) < width ? (n - s) : width;
+    const uint64_t rest = n - s - la;
+    const uint64_t lb = rest < width ? rest : width;
+    const uint64_t dl0 = d0 - s;
+    const uint64_t dl = end ? (dl0 + nv < la + lb ? dl0 + nv : la + lb) : dl0;
+    return diag_search_warp<KT>(src + s, la, src + s + la, lb, dl, lane);
+  }
+  __device__ __forceinline__ TileWin window(uint64_t t, uint64_t a0, uint64_t a1) const {
+    const uint64_t d0 = t * nv;
+    const uint64_t s = round_pair_start(t, nv, tshift);
+    const uint64_t la = (n - s) < width ? (n - s) : width;
+    const uint64_t rest = n - s - la;
+    const uint64_t lb = rest < width ? rest : width;
+    const uint64_t dl0 = d0 - s;
+    const uint64_t dl1 = dl0 + nv < la + lb ? dl0 + nv : la + lb;
     TileWin w;
     w.a0 = s + a0;
     w.b0 = s + la + (dl0 - a0);
@@ -509,7 +610,20 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
   const int tid = threadIdx.x;
 
-  const TileWin win = map.window(tile0 + blockIdx.x);
+  TileWin win;
+  if constexpr (map_searches<Map>::value) {
+    __shared__ unsigned long long split[2];
+    if (tid < 64) {  // warp 0: the tile's start diagonal, warp 1: its end
+      const int w = tid >> 5;
+      const uint64_t sp = map.template split<KT>(a, b, tile0 + blockIdx.x, w, tid & 31);
+      if ((tid & 31) == 0)
+        split[w] = sp;
+    }
+    __syncthreads();
+    win = map.window(tile0 + blockIdx.x, split[0], split[1]);
+  } else {
+    win = map.window(tile0 + blockIdx.x);
+  }
   const int na_t = win.na, nb_t = win.nb, total = na_t + nb_t;
 
   // --- smem layout (byte offsets): each window congruent mod 16 to its
