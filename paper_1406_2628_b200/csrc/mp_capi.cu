@@ -542,15 +542,6 @@ int block_sort_engine() {
   return e;
 }
 
-// K3w's levels above the warp: bitonic stages through smem (default) or
-// Merge Path passes (MP_K3W=merge), see mp_bsort.cuh.
-bool k3w_cross_warp_bitonic() {
-  static const bool b = [] {
-    const char *v = std::getenv("MP_K3W");
-    return !(v && std::strcmp(v, "merge") == 0);
-  }();
-  return b;
-}
 
 // The 16-keys-per-thread block sort: K3w (default: warp bitonic levels +
 // Merge Path passes in smem) or K3t (MP_K3W=tr: the whole bitonic network

@@ -931,3 +931,24 @@ def test_extreme_keys_merge_and_sort(cuda, port, S):
         want_s, _, _ = port.merge_sort(S, d)
         got_s = mp.parallel_merge_sort(to_dev(d, S, cuda), 4, key_type=key_type(S))
         assert same(from_dev(got_s, S), want_s)
+
+
+@pytest.mark.parametrize("fuse_tiles", ["0", "2"])
+def test_split_search_paths_vs_oracle(cuda, fuse_tiles):
+    """Merges and sorts up to one wave of CTAs search their own split
+    points in-kernel (SearchMap / RoundSearchMap, no K1/K4 launch).  Re-run
+    the random merge / sort / checksum parity tests with that path off
+    (MP_MERGE_FUSE_TILES=0: K1/K4 + K2 at every size) and with a 2-tile
+    threshold (the shapes straddle it), in a subprocess because the switch
+    is read once per process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_parity.py"),
+                        "-q", "-x", "-p", "no:cacheprovider", "-k",
+                        "random_merges or random_sorts or sort_with_values or checksum_vs"],
+                       capture_output=True, text=True, timeout=1200, cwd=str(root),
+                       env=dict(os.environ, MP_MERGE_FUSE_TILES=fuse_tiles))
+    assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
