@@ -212,15 +212,19 @@ template <class KT> uint64_t merge_ws_bytes(uint64_t n) {
   return (merge_tiles<KT>(n) + 1 + fine) * sizeof(uint64_t);
 }
 
-// Merges of at most this many plan tiles run as ONE kernel: each K2 CTA
-// searches its own split points (SearchMap), no K1 launch.  One wave of
-// 512-thread CTAs at 4 per SM on 148 SMs; beyond it every extra wave would
-// pay the search latency again.  B200, config 1 (2^20 + 2^20 u32): see
-// DESIGN.md.  MP_MERGE_FUSE_TILES overrides (0 = always K1 + K2).
+// Merges (and sort rounds) of at most this many tiles run as ONE kernel:
+// each K2 CTA searches its own split points (SearchMap / RoundSearchMap),
+// no K1/K4 launch.  The in-CTA search costs every CTA ~1-2 us of latency,
+// which the saved launch outweighs up to a few waves.  B200 A/B
+// (tools/small_probe.py, us per call, threshold 592 -> 3072 -> 4096):
+// merge 2^23 u32 24.6 -> 16.5, 3*2^23 54.0 -> 50.7; sort 2^23 301 -> 247,
+// 2^24 557 -> 510, 2^25 960 -> 962 -> 985 (4096 round tiles: worse);
+// always on: sort 2^28 6.97 -> 8.45 ms.  MP_MERGE_FUSE_TILES overrides
+// (0 = always K1/K4 + K2).
 uint64_t merge_fuse_tiles() {
   static const uint64_t v = [] {
     const char *e = std::getenv("MP_MERGE_FUSE_TILES");
-    return e ? static_cast<uint64_t>(std::atoll(e)) : uint64_t(592);
+    return e ? static_cast<uint64_t>(std::atoll(e)) : uint64_t(3072);
   }();
   return v;
 }

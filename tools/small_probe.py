@@ -11,7 +11,7 @@ from paper_1406_2628_b200 import _native as N
 dev = torch.device("cuda", 0)
 st = torch.cuda.current_stream()
 res = {}
-for n in (1 << 16, 1 << 18, 1 << 20, 1 << 22):
+for n in [int(x) for x in __import__("os").environ.get("SIZES", "65536,262144,1048576,4194304").split(",")]:
     x = torch.randint(0, 2**31 - 1, (n,), dtype=torch.int64, device=dev).to(torch.int32)
     y = torch.empty_like(x)
     sb = N.lib.mp_sort_scratch_bytes(N.KEY_U32, 0, n)
