@@ -228,6 +228,17 @@ uint64_t merge_fuse_tiles() {
   }();
   return v;
 }
+// K4 with a warp per tile boundary up to this many tiles (MP_K4_WARP_TILES):
+// B200 sort (tools/small_probe.py), us: 2^25 (4096 round tiles) 961 -> 921,
+// but 2^26 (8192) 1776 -> 1862 and 2^27 3454 -> 3805 -- the warp search's
+// 32x sectors cost more than its latency saves once K4 has many tiles.
+uint64_t k4_warp_tiles() {
+  static const uint64_t v = [] {
+    const char *e = std::getenv("MP_K4_WARP_TILES");
+    return e ? static_cast<uint64_t>(std::atoll(e)) : uint64_t(4096);
+  }();
+  return v;
+}
 template <class KT> bool merge_fused(uint64_t n) {
   return cdiv(n, uint64_t(MergeCfg<KT>::NT) * MergeCfg<KT>::VT) <= merge_fuse_tiles();
 }
@@ -623,6 +634,13 @@ int sort_rounds_from(typename KT::T *src, uint32_t *srcv, typename KT::T *dst,
     auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
       if (hi <= lo)
         return MP_OK;
+      if (lo == 0 && tiles <= k4_warp_tiles()) {
+        round_partition_warp_kernel<KT>
+            <<<static_cast<unsigned>(cdiv(hi * 32, 256)), 256, 0, st>>>(
+                src, n, w, tshift, NV, hi, P);
+        MP_LAUNCHED("round_partition_warp_kernel");
+        return MP_OK;
+      }
       round_partition_kernel<KT>
           <<<static_cast<unsigned>(cdiv(hi - lo, 128)), 128, 0, st>>>(
               src, n, w, tshift, NV, hi, P, lo);

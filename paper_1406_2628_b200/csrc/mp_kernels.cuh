@@ -374,6 +374,29 @@ __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
     P[t] = diag_search_grid<KT, MP_K4_GRID>(src + s, la, src + s + la, lb, d0 - s);
 }
 
+// K4 with one warp per tile boundary (diag_search_warp: ~log32 dependent
+// rounds of 32 parallel probes instead of ~log2 single probes): for rounds
+// whose K4 is latency-bound rather than bound by its DRAM sectors (a warp
+// reads ~32x the sectors of a single-thread search).
+template <class KT>
+__global__ void round_partition_warp_kernel(const typename KT::T *__restrict__ src,
+                                            uint64_t n, uint64_t width, uint32_t tshift,
+                                            uint32_t nv, uint64_t tiles,
+                                            uint64_t *__restrict__ P) {
+  const uint64_t t = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= tiles)
+    return;
+  const uint64_t d0 = t * nv;
+  const uint64_t s = round_pair_start(t, nv, tshift);
+  const uint64_t la = (n - s) < width ? (n - s) : width;
+  const uint64_t rest = n - s - la;
+  const uint64_t lb = rest < width ? rest : width;
+  const uint64_t a = diag_search_warp<KT>(src + s, la, src + s + la, lb, d0 - s, lane);
+  if (lane == 0)
+    P[t] = a;
+}
+
 // ---------------------------------------------------------------------------
 // K2: tile merge.
 // ---------------------------------------------------------------------------

@@ -933,14 +933,15 @@ def test_extreme_keys_merge_and_sort(cuda, port, S):
         assert same(from_dev(got_s, S), want_s)
 
 
-@pytest.mark.parametrize("fuse_tiles", ["0", "2"])
-def test_split_search_paths_vs_oracle(cuda, fuse_tiles):
-    """Merges and sorts up to one wave of CTAs search their own split
-    points in-kernel (SearchMap / RoundSearchMap, no K1/K4 launch).  Re-run
-    the random merge / sort / checksum parity tests with that path off
-    (MP_MERGE_FUSE_TILES=0: K1/K4 + K2 at every size) and with a 2-tile
-    threshold (the shapes straddle it), in a subprocess because the switch
-    is read once per process."""
+@pytest.mark.parametrize("fuse_tiles,k4_warp", [("0", "0"), ("2", "0"), ("0", "1000000")])
+def test_split_search_paths_vs_oracle(cuda, fuse_tiles, k4_warp):
+    """Merges and sorts up to a few waves of CTAs search their own split
+    points in-kernel (SearchMap / RoundSearchMap, no K1/K4 launch), and
+    somewhat larger sort rounds run K4 with a warp per boundary.  Re-run the
+    random merge / sort / checksum parity tests with the in-kernel search off
+    (MP_MERGE_FUSE_TILES=0: K1/K4 + K2 at every size), with a 2-tile
+    threshold (the shapes straddle it) and with the warp K4 for every round,
+    in a subprocess because the switches are read once per process."""
     import os
     import subprocess
     import sys
@@ -950,5 +951,6 @@ def test_split_search_paths_vs_oracle(cuda, fuse_tiles):
                         "-q", "-x", "-p", "no:cacheprovider", "-k",
                         "random_merges or random_sorts or sort_with_values or checksum_vs"],
                        capture_output=True, text=True, timeout=1200, cwd=str(root),
-                       env=dict(os.environ, MP_MERGE_FUSE_TILES=fuse_tiles))
+                       env=dict(os.environ, MP_MERGE_FUSE_TILES=fuse_tiles,
+                                MP_K4_WARP_TILES=k4_warp))
     assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
