@@ -155,6 +155,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
+// Programmatic dependent launch (PDL).  A kernel launched with the
+// programmatic-stream-serialization attribute may become resident before
+// the previous kernel in its stream has finished; pdl_wait() (griddepcontrol
+// .wait) blocks until that kernel has completed and its memory is visible,
+// and is a no-op for a normal launch.  pdl_launch_dependents() lets the next
+// such kernel launch once every CTA of this grid has started.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // MP_BULK_EVICT_FIRST (compile-time A/B): the streamed windows and tiles
 // carry an L2 evict_first policy (createpolicy + .L2::cache_hint).  B200:
 // config 2 0.650 -> 0.650/0.678 ms, config 5 5.38 -> 5.42 ms, config 4

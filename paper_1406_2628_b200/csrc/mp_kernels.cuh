@@ -135,6 +135,7 @@ __global__ void partition_kernel(const typename KT::T *__restrict__ a,
                                  uint64_t count, uint64_t *__restrict__ a_offs,
                                  unsigned long long *__restrict__ cmp = nullptr,
                                  uint64_t t0 = 0) {
+  pdl_launch_dependents();  // K2 may become resident while the searches run
   const uint64_t t = t0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (t >= count)
     return;
@@ -357,6 +358,8 @@ __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
                                        uint64_t tiles,
                                        uint64_t *__restrict__ P,
                                        uint64_t t0 = 0) {
+  pdl_wait();  // the round's input is the previous kernel's output
+  pdl_launch_dependents();
   const uint64_t t = t0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (t >= tiles)
     return;
@@ -632,6 +635,8 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
   extern __shared__ __align__(128) char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
   const int tid = threadIdx.x;
+  pdl_wait();  // split points / inputs come from the previous kernel
+  pdl_launch_dependents();
 
   TileWin win;
   if constexpr (map_searches<Map>::value) {
