@@ -643,7 +643,7 @@ template <class KT, bool VALS> uint32_t sort_round_tile() {
   if (r0 == kBareRun)
     return static_cast<uint32_t>(kBareRun);
   if (sizeof(typename KT::T) == 4 && !VALS && KT::kind != kElement && r0 % kBigTile4 == 0 &&
-      sort_big_tile_env() && !sort_quad_env())
+      sort_big_tile_env())
     return kBigTile4;
   return SortMergeCfg<KT>::TILE;
 }
@@ -877,16 +877,29 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
         MP_LAUNCHED("quad_refine_kernel");
         return MP_OK;
       };
-      int rc = NV == kBareRun ? launch(std::integral_constant<uint32_t, uint32_t(kBareRun)>{})
-                              : launch(std::integral_constant<uint32_t, 4096u>{});
+      int rc = NV == kBareRun    ? launch(std::integral_constant<uint32_t, uint32_t(kBareRun)>{})
+               : NV == kBigTile4 ? launch(std::integral_constant<uint32_t, kBigTile4>{})
+                                 : launch(std::integral_constant<uint32_t, 4096u>{});
       if (rc)
         return rc;
-      static_assert(NT * VT >= 4352 + 2 * VT, "K5e: a tile's two inner merges fit the CTA");
-      constexpr uint32_t qsmem = merge_smem_bytes<KT, false, NT, VT>();
-      auto qkern = quad_tile_kernel<KT, NT, VT>;
-      MP_CUDA(set_smem(qkern, qsmem));
-      qkern<<<static_cast<unsigned>(qtiles), NT, qsmem, s>>>(src, dst, n, w, NV, QQ);
-      MP_LAUNCHED("quad_tile_kernel");
+      const uint32_t lg4w = ((4 * w) & (4 * w - 1)) == 0
+                                ? static_cast<uint32_t>(__builtin_ctzll(4 * w))
+                                : ~0u;
+      auto tiles_k5 = [&](auto nt_tag) -> int {
+        constexpr int QNT = decltype(nt_tag)::value;
+        static_assert(QNT * VT >= 4352 + 2 * VT, "K5e: a tile's two inner merges fit the CTA");
+        constexpr uint32_t qsmem = quad_smem_bytes<KT, QNT, VT>();
+        auto qkern = quad_tile_kernel<KT, QNT, VT>;
+        MP_CUDA(set_smem(qkern, qsmem));
+        qkern<<<static_cast<unsigned>(qtiles), QNT, qsmem, s>>>(src, dst, n, w, lg4w, NV, QQ);
+        MP_LAUNCHED("quad_tile_kernel");
+        return MP_OK;
+      };
+      static_assert(kBigTileNT * VT >= int(kBigTile4) + 2 * VT, "K5e at the 8192-output tile");
+      rc = NV == kBigTile4 ? tiles_k5(std::integral_constant<int, kBigTileNT>{})
+                           : tiles_k5(std::integral_constant<int, NT>{});
+      if (rc)
+        return rc;
       std::swap(src, dst);
     }
   }

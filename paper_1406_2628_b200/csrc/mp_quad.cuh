@@ -298,11 +298,26 @@ __global__ void quad_refine_kernel(const typename KT::T *__restrict__ src, uint6
 // K5e: one CTA per tile of T outputs (NT*VT >= T + 2*VT).  Phase 1 deals
 // ceil(nx/VT) threads to X = merge(R0w, R1w) and the rest to Y; both are
 // written over their input windows; phase 2 merges X with Y.
+// Every merge runs bounds-free on sentinels (serial_merge SENT, as K2):
+// VT copies of the largest key behind each A-side window (R0w, R2w, then
+// X) and one behind each B-side window (R1w, R3w, then Y).  The group of a
+// tile is pos >> lg4w (4w is a power of two).  B200 source counters before
+// (tools/ncu_src_capture.sh): 57.2 instructions per element, of which 6.8
+// in warp 0's 64-bit window setup and 5.6 in bounds-checked tail merges.
+template <class KT, int VT>
+__host__ __device__ constexpr uint32_t quad_gap_bytes() {
+  return (VT + 1) * sizeof(typename KT::T) + 16;
+}
+template <class KT, int NT, int VT>
+__host__ __device__ constexpr uint32_t quad_smem_bytes() {
+  return 64 + NT * VT * sizeof(typename KT::T) + 4 * quad_gap_bytes<KT, VT>() + 64;
+}
+
 template <class KT, int NT, int VT>
 __global__ void __launch_bounds__(NT, 1536 / NT)
     quad_tile_kernel(const typename KT::T *__restrict__ src,
                      typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
-                     uint32_t T, const QuadPt *__restrict__ Q) {
+                     uint32_t lg4w, uint32_t T, const QuadPt *__restrict__ Q) {
   using T_ = typename KT::T;
   constexpr uint32_t KS = sizeof(T_);
   extern __shared__ __align__(128) char smem[];
@@ -318,7 +333,9 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
   if (tid < 32) {
     const uint64_t t = blockIdx.x;
     const uint64_t pos = t * T;
-    const uint64_t g = pos / (4 * w);
+    // 4w is a power of two after K3w's runs (lg4w < 64); K3b's 4352-key
+    // runs are not (lg4w = ~0u): divide
+    const uint64_t g = lg4w < 64 ? (pos >> lg4w) : pos / (4 * w);
     const QuadGroup q = quad_group(g, n, w);
     const QuadPt p0 = Q[t];
     QuadPt p1;
@@ -339,7 +356,7 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
       cnt[r] = static_cast<int>(p1.i[r] - p0.i[r]);
       gW[r] = reinterpret_cast<const char *>(src + q.S + r * w + p0.i[r]);
       oW[r] = mirror_off(at, gW[r]);
-      at = oW[r] + cnt[r] * KS;
+      at = oW[r] + cnt[r] * KS + quad_gap_bytes<KT, VT>();
     }
     const int l = tid;
     if (l == 0) {
@@ -367,6 +384,14 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
     for (int r = 0; r < 4; ++r)
       if ((l >> 3) == r)
         stage_edges<KS>(smem, oW[r], gW[r], cnt[r] * KS, l & 7);
+    // sentinels behind the windows (outside every bulk-copy destination)
+    if (l < VT) {
+      *reinterpret_cast<T_ *>(smem + oW[0] + (cnt[0] + l) * KS) = KT::max_key();
+      *reinterpret_cast<T_ *>(smem + oW[2] + (cnt[2] + l) * KS) = KT::max_key();
+    } else if (l == VT) {
+      *reinterpret_cast<T_ *>(smem + oW[1] + cnt[1] * KS) = KT::max_key();
+      *reinterpret_cast<T_ *>(smem + oW[3] + cnt[3] * KS) = KT::max_key();
+    }
   }
   __syncthreads();
   uint32_t oW[4];
@@ -400,11 +425,11 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
       else
         lo = mid + 1;
     }
-    serial_merge<KT, VT, false>(smem, oA, na, oB, nb, 0, 0, lo, d1 - lo, keys, vals);
+    serial_merge<KT, VT, false, true>(smem, oA, na, oB, nb, 0, 0, lo, d1 - lo, keys, vals);
   }
   __syncthreads();  // every window consumed
   // X over [oW0, oW0 + nx), Y over [oW2, oW2 + ny): each fits in the span
-  // of the two windows it was merged from
+  // of the two windows (and gaps) it was merged from, sentinels included
   const uint32_t oX = oW[0], oY = oW[2];
   if (act1) {
     const uint32_t op = side ? oY : oX;
@@ -420,6 +445,13 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
           *reinterpret_cast<T_ *>(smem + op + (d1 + k) * KS) = keys[k];
     }
   }
+  if (tid >= NT - 32) {  // the last warp: X's VT sentinels and Y's one
+    const int l = tid - (NT - 32);
+    if (l < VT)
+      *reinterpret_cast<T_ *>(smem + oX + (nx + l) * KS) = KT::max_key();
+    else if (l == VT)
+      *reinterpret_cast<T_ *>(smem + oY + ny * KS) = KT::max_key();
+  }
   __syncthreads();
 
   // ---- phase 2: out = merge(X, Y), ties to X ----
@@ -434,7 +466,7 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
       else
         lo = mid + 1;
     }
-    serial_merge<KT, VT, false>(smem, oX, nx, oY, ny, 0, 0, lo, d2 - lo, keys, vals);
+    serial_merge<KT, VT, false, true>(smem, oX, nx, oY, ny, 0, 0, lo, d2 - lo, keys, vals);
   }
   __syncthreads();  // X and Y consumed
 
