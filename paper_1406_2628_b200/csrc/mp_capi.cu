@@ -172,6 +172,20 @@ constexpr int kWarpNT = MP_WARP_NT;
 constexpr uint64_t kWarpRun = kWarpNT * 16;
 constexpr uint32_t kBigTile4 = 8192;  // round tile after K3w (sort_round_tile)
 constexpr int kBigTileNT = 384;       // 384 x 23 >= 8192
+// K5e (fused two-round pass) thread shape at the 8192-output tile:
+// QNT * QVT >= 8192 + 2 * QVT, QVT odd
+// B200 A/B (tools/ab_qshape.sh, whole 2^30 sort): 384 x 23 29.49 ms,
+// 288 x 31 29.11, 320 x 27 29.01
+#ifndef MP_QUAD_NT
+#define MP_QUAD_NT 320
+#endif
+#ifndef MP_QUAD_VT
+#define MP_QUAD_VT 27
+#endif
+constexpr int kQuadNT = MP_QUAD_NT;
+constexpr int kQuadVT = MP_QUAD_VT;
+static_assert(kQuadNT * kQuadVT >= int(kBigTile4) + 2 * kQuadVT && (kQuadVT & 1),
+              "K5e at the 8192-output tile");
 
 // Launch with programmatic dependent launch (mp_common.cuh pdl_*): the
 // kernel may become resident while the previous kernel of the stream drains
@@ -621,16 +635,19 @@ template <class KT, bool VALS> uint64_t sort_run0() {
     return kWarpRun;
   return kRun;
 }
-bool sort_quad_env() {
-  static const bool b = [] {
+// Fused two-round passes (mp_quad.cuh) for bare 32-bit sorts whose rounds
+// are too large for the in-kernel split search: default on, MP_SORT_QUAD=0
+// turns them off (=1 forces them at every size).
+int sort_quad_env() {
+  static const int v = [] {
     const char *e = std::getenv("MP_SORT_QUAD");
-    return e && std::strcmp(e, "1") == 0;
+    return !e ? 2 : std::strcmp(e, "0") == 0 ? 0 : 1;
   }();
-  return b;
+  return v;
 }
 // Round tile after K3w's 8192-key runs: kBigTile4 (8192 = 384 threads x 23
 // outputs: half the K4 split searches of 4096-output tiles) unless
-// MP_SORT_TILE=4096 or the fused two-round pass (grid G = tile) is on.
+// MP_SORT_TILE=4096.
 bool sort_big_tile_env() {
   static const bool b = [] {
     const char *e = std::getenv("MP_SORT_TILE");
@@ -766,13 +783,17 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   int rounds = 0;
   for (uint64_t w = run0; w < n; w *= 2)
     ++rounds;
-  // MP_SORT_QUAD=1: fuse round pairs into one HBM pass (mp_quad.cuh).
-  // Opt-in: bit-exact, but measured on B200 (2^30 u32, per fused pass):
-  // K4q 0.18 + K4r 0.43 + K5e 2.41 = 3.0 ms vs 2 x (1.25 + 0.10) ms for two
-  // plain rounds -- K5e halves the HBM bytes but issues 57 instructions per
-  // element (two searches + two serial merges), so it is issue-bound above
-  // the time of the two HBM-bound rounds it replaces.
-  const bool use_quad = (use_bare || use_warp) && sort_quad_env();
+  // Fused round pairs: one HBM pass per two rounds (mp_quad.cuh).  B200,
+  // 2^30 u32, per pass at the 8192-output tile: K4q 0.11 + K4r 0.28 + K5e
+  // 2.07 ms (41.7 instructions per element, 320 x 27 threads) vs 2 x
+  // (1.23 + 0.06) ms for two plain rounds; with half the HBM traffic the
+  // sort also stays under the power cap: 29.0 vs 30.6 ms on one box.  Small
+  // sorts keep the plain rounds (their in-kernel split search is cheaper
+  // than K4q + K4r).
+  const int quad_mode = (use_bare || use_warp) ? sort_quad_env() : 0;
+  const bool use_quad =
+      quad_mode == 1 ||
+      (quad_mode == 2 && cdiv(n, uint64_t(sort_round_tile<KT, VALS>())) > merge_fuse_tiles());
   const int quad_passes = use_quad ? rounds / 2 : 0;
   const int passes = rounds - quad_passes;  // ping-pong swaps after the block sort
   // Block sort lands where an even/odd number of ping-pong passes ends in
@@ -887,16 +908,16 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
                                 : ~0u;
       auto tiles_k5 = [&](auto nt_tag) -> int {
         constexpr int QNT = decltype(nt_tag)::value;
-        static_assert(QNT * VT >= 4352 + 2 * VT, "K5e: a tile's two inner merges fit the CTA");
-        constexpr uint32_t qsmem = quad_smem_bytes<KT, QNT, VT>();
-        auto qkern = quad_tile_kernel<KT, QNT, VT>;
+        constexpr int QVT = QNT == kQuadNT ? kQuadVT : VT;
+        static_assert(QNT * QVT >= 4352 + 2 * QVT, "K5e: a tile's two inner merges fit the CTA");
+        constexpr uint32_t qsmem = quad_smem_bytes<KT, QNT, QVT>();
+        auto qkern = quad_tile_kernel<KT, QNT, QVT>;
         MP_CUDA(set_smem(qkern, qsmem));
         qkern<<<static_cast<unsigned>(qtiles), QNT, qsmem, s>>>(src, dst, n, w, lg4w, NV, QQ);
         MP_LAUNCHED("quad_tile_kernel");
         return MP_OK;
       };
-      static_assert(kBigTileNT * VT >= int(kBigTile4) + 2 * VT, "K5e at the 8192-output tile");
-      rc = NV == kBigTile4 ? tiles_k5(std::integral_constant<int, kBigTileNT>{})
+      rc = NV == kBigTile4 ? tiles_k5(std::integral_constant<int, kQuadNT>{})
                            : tiles_k5(std::integral_constant<int, NT>{});
       if (rc)
         return rc;
