@@ -313,6 +313,35 @@ __host__ __device__ constexpr uint32_t quad_smem_bytes() {
   return 64 + NT * VT * sizeof(typename KT::T) + 4 * quad_gap_bytes<KT, VT>() + 64;
 }
 
+// MP_QUAD_FIXED_SEARCH=1 (compile-time A/B): K5e's splits by fixed-step
+// binary lifting instead of the while loop.  B200: 1.35 vs 1.40 G
+// instructions but K5e 2.30 vs 2.07 ms (sort 30.8 vs 29.0 ms) -- every
+// warp now pays the longest chain of 13 dependent probe pairs.  Off.
+#ifndef MP_QUAD_FIXED_SEARCH
+#define MP_QUAD_FIXED_SEARCH 0
+#endif
+// Split of the smem windows A[0, na), B[0, nb) on diagonal d (core.hpp:110
+// predicate, ties to A) by binary lifting with a fixed number of steps K
+// (2^K > min(na, nb)): no loop branch, no divergence between lanes.  Probe
+// indices are clamped into the windows' neighbourhood; a clamped probe never
+// moves the answer.
+template <class KT, int K>
+__device__ __forceinline__ int split_fixed(const char *smem, uint32_t oA, int na,
+                                           uint32_t oB, int nb, int d) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  int i = d > nb ? d - nb : 0;
+  const int hi = d < na ? d : na;
+#pragma unroll
+  for (int step = 1 << (K - 1); step > 0; step >>= 1) {
+    const int j = i + step;  // does the split lie at or beyond j?
+    const int jj = j < hi ? j : hi;
+    const bool stay = take_b<KT>(lds<T>(smem, oB + (d - jj) * KS), lds<T>(smem, oA + (jj - 1) * KS));
+    i = (j <= hi && !stay) ? j : i;
+  }
+  return i;
+}
+
 template <class KT, int NT, int VT>
 __global__ void __launch_bounds__(NT, 1536 / NT)
     quad_tile_kernel(const typename KT::T *__restrict__ src,
@@ -416,6 +445,10 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
   const int d1 = t1 * VT;
   const bool act1 = d1 < na + nb;
   if (act1) {
+#if MP_QUAD_FIXED_SEARCH
+    // min(na, nb) <= T / 2 <= 2^13 - 1 for tiles up to 16382 outputs
+    const int lo = split_fixed<KT, 13>(smem, oA, na, oB, nb, d1);
+#else
     int lo = d1 > nb ? d1 - nb : 0;
     int hi = d1 < na ? d1 : na;
     while (lo < hi) {
@@ -425,6 +458,7 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
       else
         lo = mid + 1;
     }
+#endif
     serial_merge<KT, VT, false, true>(smem, oA, na, oB, nb, 0, 0, lo, d1 - lo, keys, vals);
   }
   __syncthreads();  // every window consumed
@@ -457,6 +491,9 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
   // ---- phase 2: out = merge(X, Y), ties to X ----
   const int d2 = tid * VT;
   if (d2 < total) {
+#if MP_QUAD_FIXED_SEARCH
+    const int lo = split_fixed<KT, 13>(smem, oX, nx, oY, ny, d2);
+#else
     int lo = d2 > ny ? d2 - ny : 0;
     int hi = d2 < nx ? d2 : nx;
     while (lo < hi) {
@@ -466,6 +503,7 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
       else
         lo = mid + 1;
     }
+#endif
     serial_merge<KT, VT, false, true>(smem, oX, nx, oY, ny, 0, 0, lo, d2 - lo, keys, vals);
   }
   __syncthreads();  // X and Y consumed
