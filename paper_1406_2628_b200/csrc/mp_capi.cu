@@ -184,6 +184,17 @@ constexpr int kBigTileNT = 384;       // 384 x 23 >= 8192
 #endif
 constexpr int kQuadNT = MP_QUAD_NT;
 constexpr int kQuadVT = MP_QUAD_VT;
+// K5e2 (two merge slots per thread): 2 * kQuad2NT * kQuadVT >= 8192 + 2 * kQuadVT.
+// Compile-time A/B: B200 K5e2 (160 x 2 x 27) 2.50 ms vs K5e (320 x 27) 2.07
+// ms per pass -- 72 registers leave 25 warps per SM and the second chain
+// does not make up for them.  Off.
+#ifndef MP_QUAD_ILP2
+#define MP_QUAD_ILP2 0
+#endif
+#ifndef MP_QUAD2_NT
+#define MP_QUAD2_NT 160
+#endif
+constexpr int kQuad2NT = MP_QUAD2_NT;
 static_assert(kQuadNT * kQuadVT >= int(kBigTile4) + 2 * kQuadVT && (kQuadVT & 1),
               "K5e at the 8192-output tile");
 
@@ -917,8 +928,24 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
         MP_LAUNCHED("quad_tile_kernel");
         return MP_OK;
       };
+#if MP_QUAD_ILP2
+      if (NV == kBigTile4) {
+        // two merge slots per thread (quad_tile2_kernel)
+        constexpr int Q2NT = kQuad2NT, Q2VT = kQuadVT;
+        static_assert(2 * Q2NT * Q2VT >= int(kBigTile4) + 2 * Q2VT, "K5e2 covers the tile");
+        constexpr uint32_t qsmem = quad2_smem_bytes<KT, Q2NT, Q2VT>();
+        auto qkern = quad_tile2_kernel<KT, Q2NT, Q2VT>;
+        MP_CUDA(set_smem(qkern, qsmem));
+        qkern<<<static_cast<unsigned>(qtiles), Q2NT, qsmem, s>>>(src, dst, n, w, lg4w, NV, QQ);
+        MP_LAUNCHED("quad_tile2_kernel");
+        rc = MP_OK;
+      } else {
+        rc = tiles_k5(std::integral_constant<int, NT>{});
+      }
+#else
       rc = NV == kBigTile4 ? tiles_k5(std::integral_constant<int, kQuadNT>{})
                            : tiles_k5(std::integral_constant<int, NT>{});
+#endif
       if (rc)
         return rc;
       std::swap(src, dst);
