@@ -540,7 +540,7 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
   if (tiles >= (1ull << 31))
     return fail(MP_ERR_INVALID, "merge too large (%llu elements)",
                 (unsigned long long)n);
-  if (!PEER && merge_fused<KT>(n)) {  // one wave: CTAs search their own splits
+  if (!PEER && merge_fused<KT>(n)) {  // a few waves: CTAs search their own splits
     constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
     auto kern = merge_tiles_kernel<KT, VALS, NT, VT, SearchMap, SINK>;
     MP_CUDA(set_smem(kern, smem));
@@ -625,10 +625,10 @@ int block_sort_engine() {
 // The 16-keys-per-thread block sort: K3w (default: warp bitonic levels +
 // Merge Path passes in smem) or K3t (MP_K3W=tr: the whole bitonic network
 // in registers with smem transposes), see mp_bsort.cuh.  Same runs, same
-// bytes.  B200 (2^30 u32, ncu): K3w 8.26 ms (5.9 G warp instructions, ALU
-// pipe 90.5 %), K3t 8.44 ms (5.8 G, ALU pipe 80.5 %, LSU 58.6 %) -- both
-// are bound by the ALU pipe's min/max rate (VIMNMX issues at half rate and a
-// compare-exchange whose direction depends on the lane costs two of them).
+// bytes.  B200 (2^30 u32, ncu, current code): K3w 7.80 ms (6.1 G warp
+// instructions, ALU pipe 85 %), K3t 8.10 ms (5.3 G, ALU pipe 81 %, LSU
+// 61 %) -- both bound by the ALU pipe's min/max rate (VIMNMX issues at half
+// rate and a compare-exchange whose direction depends on the lane costs two).
 bool k3w_transposed() {
   static const bool b = [] {
     const char *v = std::getenv("MP_K3W");
@@ -737,7 +737,7 @@ int sort_rounds_from(typename KT::T *src, uint32_t *srcv, typename KT::T *dst,
       MP_LAUNCHED("merge_tiles_kernel(round)");
       return MP_OK;
     };
-    if (tiles <= merge_fuse_tiles()) {  // one wave: CTAs search their own splits
+    if (tiles <= merge_fuse_tiles()) {  // a few waves: CTAs search their own splits
       auto kfs = merge_tiles_kernel<KT, VALS, NT, VT, RoundSearchMap, false>;
       MP_CUDA(set_smem(kfs, smem));
       kfs<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
