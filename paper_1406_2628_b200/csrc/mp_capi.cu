@@ -174,10 +174,12 @@ constexpr uint32_t kBigTile4 = 8192;  // round tile after K3w (sort_round_tile)
 constexpr int kBigTileNT = 384;       // 384 x 23 >= 8192
 // K5e (fused two-round pass) thread shape at the 8192-output tile:
 // QNT * QVT >= 8192 + 2 * QVT, QVT odd
-// B200 A/B (tools/ab_qshape.sh, whole 2^30 sort): 384 x 23 29.49 ms,
-// 288 x 31 29.11, 320 x 27 29.01
+// B200 A/B (tools/ab_qshape.sh, ab_q16k.sh, whole 2^30 sort): at the
+// 8192-output tile 384 x 23 29.49 ms, 288 x 31 29.11, 320 x 27 29.01; at
+// the 16384-output tile 640 x 27 28.17-28.32 (K4q + K4r per pass 0.39 ->
+// 0.18 ms, K5e 2.07 -> 2.13 ms), 544 x 31 29.28
 #ifndef MP_QUAD_NT
-#define MP_QUAD_NT 320
+#define MP_QUAD_NT 640
 #endif
 #ifndef MP_QUAD_VT
 #define MP_QUAD_VT 27
@@ -192,11 +194,17 @@ constexpr int kQuadVT = MP_QUAD_VT;
 #define MP_QUAD_ILP2 0
 #endif
 #ifndef MP_QUAD2_NT
-#define MP_QUAD2_NT 160
+#define MP_QUAD2_NT 320
 #endif
 constexpr int kQuad2NT = MP_QUAD2_NT;
-static_assert(kQuadNT * kQuadVT >= int(kBigTile4) + 2 * kQuadVT && (kQuadVT & 1),
-              "K5e at the 8192-output tile");
+// the fused pass's output tile after K3w's runs (a multiple of the round
+// tile that divides 4 x 8192)
+#ifndef MP_QUAD_TILE
+#define MP_QUAD_TILE 16384
+#endif
+constexpr uint32_t kQuadTile = MP_QUAD_TILE;
+static_assert(kQuadNT * kQuadVT >= int(kQuadTile) + 2 * kQuadVT && (kQuadVT & 1),
+              "K5e at the fused-pass tile");
 
 // Launch with programmatic dependent launch (mp_common.cuh pdl_*): the
 // kernel may become resident while the previous kernel of the stream drains
@@ -884,7 +892,10 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
     // K4r exact 4-way splits at every NV-output tile, K5e tile merges
     for (int fused_left = quad_passes; fused_left > 0 && w < n; --fused_left, w *= 4) {
       QuadPt *QP = reinterpret_cast<QuadPt *>(ws + L.quad_off);
-      const uint32_t G = NV;
+      // the fused pass's tile QT (and crossing grid) may be wider than the
+      // plain rounds' tile: kQuadTile after K3w's runs
+      const uint32_t QT = NV == kBigTile4 ? kQuadTile : NV;
+      const uint32_t G = QT;
       const uint32_t lshift = static_cast<uint32_t>(__builtin_ctzll(4 * w / G));
       const uint64_t full = n / (4 * w);
       uint64_t lines = full << lshift;
@@ -897,7 +908,7 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
         }
         lines += cdiv(l[0] + l[1], G) + cdiv(l[2] + l[3], G);
       }
-      const uint64_t qtiles = cdiv(n, NV);
+      const uint64_t qtiles = cdiv(n, QT);
       QuadPt *QQ = QP + cdiv(n, G) + 8;
       auto launch = [&](auto g_tag) -> int {
         constexpr uint32_t GG = decltype(g_tag)::value;
@@ -905,12 +916,12 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
             src, n, w, lshift, lines, QP);
         MP_LAUNCHED("quad_partition_kernel");
         quad_refine_kernel<KT, GG><<<static_cast<unsigned>(cdiv(qtiles, 128)), 128, 0, s>>>(
-            src, n, w, lshift, NV, qtiles, QP, QQ);
+            src, n, w, lshift, QT, qtiles, QP, QQ);
         MP_LAUNCHED("quad_refine_kernel");
         return MP_OK;
       };
-      int rc = NV == kBareRun    ? launch(std::integral_constant<uint32_t, uint32_t(kBareRun)>{})
-               : NV == kBigTile4 ? launch(std::integral_constant<uint32_t, kBigTile4>{})
+      int rc = QT == kBareRun    ? launch(std::integral_constant<uint32_t, uint32_t(kBareRun)>{})
+               : QT == kQuadTile ? launch(std::integral_constant<uint32_t, kQuadTile>{})
                                  : launch(std::integral_constant<uint32_t, 4096u>{});
       if (rc)
         return rc;
@@ -924,26 +935,26 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
         constexpr uint32_t qsmem = quad_smem_bytes<KT, QNT, QVT>();
         auto qkern = quad_tile_kernel<KT, QNT, QVT>;
         MP_CUDA(set_smem(qkern, qsmem));
-        qkern<<<static_cast<unsigned>(qtiles), QNT, qsmem, s>>>(src, dst, n, w, lg4w, NV, QQ);
+        qkern<<<static_cast<unsigned>(qtiles), QNT, qsmem, s>>>(src, dst, n, w, lg4w, QT, QQ);
         MP_LAUNCHED("quad_tile_kernel");
         return MP_OK;
       };
 #if MP_QUAD_ILP2
-      if (NV == kBigTile4) {
+      if (QT == kQuadTile) {
         // two merge slots per thread (quad_tile2_kernel)
         constexpr int Q2NT = kQuad2NT, Q2VT = kQuadVT;
-        static_assert(2 * Q2NT * Q2VT >= int(kBigTile4) + 2 * Q2VT, "K5e2 covers the tile");
+        static_assert(2 * Q2NT * Q2VT >= int(kQuadTile) + 2 * Q2VT, "K5e2 covers the tile");
         constexpr uint32_t qsmem = quad2_smem_bytes<KT, Q2NT, Q2VT>();
         auto qkern = quad_tile2_kernel<KT, Q2NT, Q2VT>;
         MP_CUDA(set_smem(qkern, qsmem));
-        qkern<<<static_cast<unsigned>(qtiles), Q2NT, qsmem, s>>>(src, dst, n, w, lg4w, NV, QQ);
+        qkern<<<static_cast<unsigned>(qtiles), Q2NT, qsmem, s>>>(src, dst, n, w, lg4w, QT, QQ);
         MP_LAUNCHED("quad_tile2_kernel");
         rc = MP_OK;
       } else {
         rc = tiles_k5(std::integral_constant<int, NT>{});
       }
 #else
-      rc = NV == kBigTile4 ? tiles_k5(std::integral_constant<int, kQuadNT>{})
+      rc = QT == kQuadTile ? tiles_k5(std::integral_constant<int, kQuadNT>{})
                            : tiles_k5(std::integral_constant<int, NT>{});
 #endif
       if (rc)
