@@ -22,3 +22,18 @@ def duplex():
     with torch.cuda.stream(s2): h_out.copy_(d_out, non_blocking=True)
 dup = t(duplex)
 print(json.dumps({"h2d_GBps": n/h2d/1e9, "d2h_GBps": n/d2h/1e9, "duplex_each_GBps": n/dup/1e9, "duplex_total_GBps": 2*n/dup/1e9}))
+
+# the same copies split over two streams per direction (two DMA engines?)
+s3, s4 = torch.cuda.Stream(), torch.cuda.Stream()
+hh = n // 2
+def h2d2():
+    with torch.cuda.stream(s1): d_in[:hh].copy_(h_in[:hh], non_blocking=True)
+    with torch.cuda.stream(s3): d_in[hh:].copy_(h_in[hh:], non_blocking=True)
+def d2h2():
+    with torch.cuda.stream(s2): h_out[:hh].copy_(d_out[:hh], non_blocking=True)
+    with torch.cuda.stream(s4): h_out[hh:].copy_(d_out[hh:], non_blocking=True)
+def dup2():
+    h2d2(); d2h2()
+a, b, c = t(h2d2), t(d2h2), t(dup2)
+print(json.dumps({"two_streams_h2d_GBps": n/a/1e9, "two_streams_d2h_GBps": n/b/1e9,
+                  "two_streams_duplex_each_GBps": n/c/1e9}))
