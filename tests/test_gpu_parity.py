@@ -447,6 +447,42 @@ def test_config4_sort_full_size(cuda):
     assert torch.equal(got, ref)
 
 
+@pytest.mark.parametrize("kind", ["u32", "i32", "f32"])
+def test_mid_size_sorts_with_fused_round_pairs(cuda, kind):
+    """Sizes past the in-kernel-search threshold take the fused round pairs
+    by default (K4q/K4r/K5e at 16384-output tiles): ragged sizes (short
+    last groups of 1-3 runs), uniform keys and heavy duplicates, against
+    torch.sort of the order image (bare keys: the sorted bytes are unique)."""
+    torch = _torch()
+    from paper_1406_2628_b200 import _native as N
+    st = torch.cuda.current_stream().cuda_stream
+    kt = {"u32": N.KEY_U32, "i32": N.KEY_I32, "f32": N.KEY_F32}[kind]
+    g = torch.Generator(device=cuda)
+    g.manual_seed(1406)
+    for n, span in ((30_000_001, 1 << 32), (50_331_655, 1 << 32), (41_943_040 + 8191, 977)):
+        raw = torch.randint(0, span, (n,), device=cuda, generator=g, dtype=torch.int64)
+        if kind == "f32":
+            f = (raw - span // 2).to(torch.float32) / 3.0
+            f[::97] = -0.0
+            x = f.view(torch.int32)
+        else:
+            x = (raw - (span // 2 if kind == "i32" else 0)).to(torch.int64)
+            x = (x & 0xFFFFFFFF).to(torch.int64)
+            x = torch.where(x >= 2**31, x - 2**32, x).to(torch.int32)
+        u = x.to(torch.int64) & 0xFFFFFFFF
+        if kind == "i32":
+            key = u ^ 0x80000000
+        elif kind == "f32":
+            key = torch.where(u >= 2**31, (~u) & 0xFFFFFFFF, u | 0x80000000)
+        else:
+            key = u
+        want = u[torch.sort(key, stable=True).indices]
+        y = x.clone()
+        N.check(N.lib.mp_sort(kt, y.data_ptr(), None, n, None, 0, st))
+        got = y.to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(got, want), (kind, n)
+
+
 # ------------------------------------------------------------ helpers
 def _rand_sorted(S, rng, n, dup):
     from oracle.bindings import ELEMENT_DTYPE
