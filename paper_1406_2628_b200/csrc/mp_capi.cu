@@ -194,10 +194,12 @@ constexpr int kQuadVT = MP_QUAD_VT;
 #ifndef MP_QUAD_ILP2
 #define MP_QUAD_ILP2 0
 #endif
+#if MP_QUAD_ILP2
 #ifndef MP_QUAD2_NT
 #define MP_QUAD2_NT 320
 #endif
 constexpr int kQuad2NT = MP_QUAD2_NT;
+#endif
 // the fused pass's output tile after K3w's runs (a multiple of the round
 // tile that divides 4 x 8192)
 #ifndef MP_QUAD_TILE
