@@ -144,6 +144,11 @@ __global__ void quad_partition_kernel(const typename KT::T *__restrict__ src,
 }
 
 // ---------------------------------------------------------------------------
+// K4r guess window (B200, 8 K4r launches of a 2^30 sort, ncu: 64 1061 us,
+// 128 986, 256 906, 512 1047, 1024 1186; sort 27.37 ms at 128, 27.29 at 256)
+#ifndef MP_K4R_GUESS_R
+#define MP_K4R_GUESS_R 256
+#endif
 // K4r / K5e (see the header).  An earlier variant ran one CTA per segment
 // (0..2G outputs, bimodal around G): half of every CTA idle, 3.48 ms per
 // fused pass.
@@ -266,7 +271,7 @@ __global__ void quad_refine_kernel(const typename KT::T *__restrict__ src, uint6
     // so every probe narrows the range the next inner searches scan.
     uint64_t xl = d > ny ? d - ny : 0, xh = d < nx ? d : nx;
     uint64_t aL = 0, aH = la0, cL = 0, cH = lb0;  // a(x) for x in [xl,xh]; c(y)
-    // The first two probes go to the proportional guess +- 128 instead of
+    // The first two probes go to the proportional guess +- R instead of
     // the midpoint (any probe in [xl, xh) keeps the bisection exact); for
     // random-order runs they leave a 257-wide range, ~6 probes fewer than
     // bisecting the whole segment.  B200: see DESIGN.md.
@@ -277,8 +282,9 @@ __global__ void quad_refine_kernel(const typename KT::T *__restrict__ src, uint6
     int it = 0;
     while (xl < xh) {
       uint64_t x = xl + ((xh - xl) >> 1);
-      if (it < 2 && xh - xl > 512) {
-        const uint64_t t = it == 0 ? (guess > 128 ? guess - 128 : 0) : guess + 128;
+      if (it < 2 && xh - xl > 4 * MP_K4R_GUESS_R) {
+        const uint64_t t = it == 0 ? (guess > MP_K4R_GUESS_R ? guess - MP_K4R_GUESS_R : 0)
+                                   : guess + MP_K4R_GUESS_R;
         if (t >= xl && t < xh)
           x = t;
       }
