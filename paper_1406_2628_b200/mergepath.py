@@ -163,6 +163,35 @@ def _check_p(p: int) -> None:
         raise ValueError("merge: worker count must be positive")
 
 
+# --------------------------------------------------------------------------
+# comparators: the reference templates take any Comp; the device kernels
+# implement exactly one order per key type (b200_backend.hpp key_traits).
+# The Python mirror accepts the same allow-list by name and rejects every
+# other comparator, as the C++ drop-in does at compile time.
+# --------------------------------------------------------------------------
+LESS = "less"                          # std::less<T> on u32/i32/u64/i64
+TOTAL_ORDER_LESS = "total_order_less"  # IEEE totalOrder on f32
+KEY_LESS = "key_less"                  # mergepath::key_less on element (core.hpp:52)
+
+_COMP_FOR = {N.KEY_U32: LESS, N.KEY_I32: LESS, N.KEY_U64: LESS, N.KEY_I64: LESS,
+             N.KEY_F32: TOTAL_ORDER_LESS, N.KEY_ELEMENT: KEY_LESS}
+
+
+def _check_comp(comp, kt) -> None:
+    """None selects the key type's own order.  Otherwise comp must name that
+    order (LESS / TOTAL_ORDER_LESS / KEY_LESS, or operator.lt for the
+    integer keys); a custom callable (e.g. descending) has no kernel and
+    raises TypeError instead of being ignored."""
+    if comp is None:
+        return
+    import operator
+    want = _COMP_FOR[kt]
+    if comp == want or (comp is operator.lt and want == LESS):
+        return
+    raise TypeError(f"comparator {comp!r} is not supported for this key type on the B200 "
+                    f"backend (supported: None or {want!r})")
+
+
 def _window_of(cache_elems: int) -> int:  # parallel.hpp:59-63
     if cache_elems < 3:
         raise ValueError("merge: cache capacity must be at least 3")
@@ -292,6 +321,7 @@ def parallel_merge_into(a, b, out, p: int = 1, comp=None, stats: MergeStats | No
     """parallel.hpp:151-171: stable merge of A and B into `out`."""
     _check_p(p)
     A, B = _pair(a, b, key_type)
+    _check_comp(comp, A.kt)
     _merge(A, B, out, a_vals, b_vals, out_vals)
     _merge_stats(A, B, p, stats)
 
@@ -302,6 +332,7 @@ def parallel_merge(a, b, p: int = 1, comp=None, stats: MergeStats | None = None,
     when values are given."""
     _check_p(p)
     A, B = _pair(a, b, key_type)
+    _check_comp(comp, A.kt)
     out = _empty_like_keys(A, A.n + B.n)
     out_vals = _empty_vals(A, A.n + B.n) if a_vals is not None else None
     _merge(A, B, out, a_vals, b_vals, out_vals)
@@ -368,6 +399,7 @@ def segmented_parallel_merge_into(a, b, out, p: int, cache_elems: int, comp=None
     _check_p(p)
     _window_of(cache_elems)
     A, B = _pair(a, b, key_type)
+    _check_comp(comp, A.kt)
     _merge(A, B, out, a_vals, b_vals, out_vals)
     _segmented_stats(A, B, p, cache_elems, stats)
 
@@ -379,6 +411,7 @@ def segmented_parallel_merge(a, b, p: int, cache_elems: int, comp=None,
     _check_p(p)
     _window_of(cache_elems)
     A, B = _pair(a, b, key_type)
+    _check_comp(comp, A.kt)
     out = _empty_like_keys(A, A.n + B.n)
     out_vals = _empty_vals(A, A.n + B.n) if a_vals is not None else None
     _merge(A, B, out, a_vals, b_vals, out_vals)
@@ -401,6 +434,7 @@ def parallel_merge_checksum(a, b, p: int = 1, comp=None, stats=None, key_type=No
     """parallel.hpp:181-198: register-sink merge (no output array)."""
     _check_p(p)
     A, B = _pair(a, b, key_type)
+    _check_comp(comp, A.kt)
     s = _checksum(A, B)
     _merge_stats(A, B, p, stats)
     return s
@@ -412,6 +446,7 @@ def segmented_parallel_merge_checksum(a, b, p: int, cache_elems: int, comp=None,
     _check_p(p)
     _window_of(cache_elems)
     A, B = _pair(a, b, key_type)
+    _check_comp(comp, A.kt)
     s = _checksum(A, B)
     _segmented_stats(A, B, p, cache_elems, stats)
     return s
@@ -465,6 +500,7 @@ def parallel_merge_sort(data, p: int = 1, comp=None, stats: SortStats | None = N
     reports the reference plan's round count (sort.hpp:142-146) so that
     drop-in callers see unchanged statistics."""
     _check_p(p)
+    _check_comp(comp, _Arr(data, key_type).kt)
     res = _sort(data, vals, key_type)
     if stats is not None:
         n = _Arr(data, key_type).n
@@ -477,6 +513,7 @@ def cache_efficient_parallel_sort(data, p: int, cache_elems: int, comp=None,
     """sort.hpp:150-195: same bytes as the plain sort (test_sort.cpp:128-135)."""
     _check_p(p)
     _window_of(cache_elems)
+    _check_comp(comp, _Arr(data, key_type).kt)
     res = _sort(data, vals, key_type)
     if stats is not None:
         n = _Arr(data, key_type).n

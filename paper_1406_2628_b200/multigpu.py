@@ -455,6 +455,7 @@ class P2PSorter:
     def __init__(self, capacity: int, dtype, key_type: int, group=None, device=None):
         self.comm = _Comm(group)
         self.kt = key_type
+        self.capacity = int(capacity)
         dev = device or torch.device("cuda", torch.cuda.current_device())
         words = capacity * (2 if key_type == N.KEY_ELEMENT else 1)
         wdt = torch.int64 if key_type == N.KEY_ELEMENT else dtype
@@ -473,6 +474,11 @@ class P2PSorter:
         P, me = self.comm.world, self.comm.rank
         kt = self.kt
         n_me = n_keys(x_local, kt)
+        if n_me > self.capacity:
+            # buf[0] holds `capacity` keys and is mapped into every peer:
+            # an overrun would corrupt memory the peers read
+            raise ValueError(f"P2PSorter.run: shard of {n_me} keys exceeds the capacity "
+                             f"{self.capacity} set at construction")
         lens = [x[0] for x in self.comm.all_gather_int([n_me])]
         stream = torch.cuda.current_stream(self.buf[0].device)
         st = stream.cuda_stream
@@ -503,6 +509,8 @@ class P2PSorter:
                 k = owners.index(me)
                 tot = sum(lens[q] for q in owners)
                 o0, o1 = k * tot // len(owners), (k + 1) * tot // len(owners)
+                if o1 - o0 > self.capacity:  # an equal split never exceeds the largest shard
+                    raise ValueError("P2PSorter.run: round slice exceeds the capacity")
                 pa = N.pieces_array([(self.peer[q][cur] if lens[q] else None, None, lens[q])
                                      for q in left])
                 pb = N.pieces_array([(self.peer[q][cur] if lens[q] else None, None, lens[q])

@@ -116,3 +116,36 @@ def test_sort_plan_kats(kats):
                 assert getattr(plan, key) == c[key], c["src"]
     gp = mp.gpu_sort_plan(1 << 30)
     assert gp.block_size == 2048 and gp.tree_levels == 19
+
+
+def test_custom_comparator_rejected():
+    """A comparator the kernels do not implement raises instead of being
+    ignored (the C++ drop-in rejects it at compile time, b200_backend.hpp)."""
+    import operator
+    from paper_1406_2628_b200 import mergepath as mp
+    a = np.arange(4, dtype=np.uint32)
+    desc = lambda x, y: x > y  # noqa: E731
+    for call in (lambda c: mp.parallel_merge(a, a, 2, comp=c),
+                 lambda c: mp.parallel_merge_into(a, a, np.empty(8, np.uint32), 2, comp=c),
+                 lambda c: mp.segmented_parallel_merge(a, a, 2, 30, comp=c),
+                 lambda c: mp.parallel_merge_checksum(a, a, 2, comp=c),
+                 lambda c: mp.parallel_merge_sort(a, 2, comp=c),
+                 lambda c: mp.cache_efficient_parallel_sort(a, 2, 30, comp=c)):
+        with pytest.raises(TypeError):
+            call(desc)
+        with pytest.raises(TypeError):
+            call(mp.TOTAL_ORDER_LESS)  # the f32 order on u32 keys
+    f = np.zeros(2, dtype=np.float32)
+    with pytest.raises(TypeError):
+        mp.parallel_merge(f, f, 1, comp=operator.lt)  # std::less<float>: -0 == +0
+    # the allow-listed names pass the check (then fail loudly without a GPU)
+    mp._check_comp(mp.LESS, N_KEY("u32"))
+    mp._check_comp(operator.lt, N_KEY("i64"))
+    mp._check_comp(mp.TOTAL_ORDER_LESS, N_KEY("f32"))
+    mp._check_comp(mp.KEY_LESS, N_KEY("element"))
+
+
+def N_KEY(name):
+    from paper_1406_2628_b200 import _native as N
+    return {"u32": N.KEY_U32, "i64": N.KEY_I64, "f32": N.KEY_F32,
+            "element": N.KEY_ELEMENT}[name]
