@@ -65,6 +65,18 @@ CONFIGS = {
 BARE_RUN = 8192  # mp_sort's block-sort run for bare 32-bit keys (K3w: 512 threads x 16)
 
 
+def config_dict(cfg, ws):
+    """The `config` object of a line -- identical for both arms (the
+    reference arm's CPU thread count is in its cpu_baseline)."""
+    units = cfg["n"] if cfg["kind"] == "sort" else cfg["na"] + cfg["nb"]
+    alg = units * cfg["bytes_per"]
+    return {"workload": cfg["desc"],
+            "l2": ("inputs+output larger than L2 (no flush needed)" if alg > 4 * 126e6
+                   else "fits in L2 (warm)"),
+            "parallelism": f"dp{ws}" if ws > 1 else "single GPU",
+            "elements_per_gpu": units}
+
+
 def sort_rounds(n: int, run: int = BARE_RUN) -> int:
     """Merge rounds of mp_sort after the block sort (runs double per round)."""
     r, w = 0, run
@@ -302,10 +314,7 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
         "vs_baseline": None, "dtype": key,
         "data": "synthetic: SplitMix64 counter generator x_i=mix64(seed+i*0x9E3779B97F4A7C15), "
                 "sorted ascending before timing",
-        "config": {"workload": cfg["desc"], "l2": "inputs+output larger than L2 "
-                   "(no flush needed)" if alg_bytes > 4 * 126e6 else "fits in L2 (warm)",
-                   "parallelism": f"dp{ws}" if ws > 1 else "single GPU",
-                   "elements_per_gpu": units},
+        "config": config_dict(cfg, ws),
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
@@ -420,14 +429,15 @@ def host_inputs(cfg):
     return a, b
 
 
-def time_reference(cfg, ha, hb, reps, budget_s, sample_frac=None):
+def time_reference(cfg, ha, hb, reps, budget_s, sample_frac=None, p=None):
     """Time the reference's own CPU path: parallel_merge_into with a warm
     thread_team(p = host cores) (parallel.hpp:151-162), or
     parallel_merge_sort(span, p) (sort.hpp:132-148).  Returns
-    (elements per second, seconds per rep, p, sample description, out)."""
+    (elements per second, seconds per rep, p, sample description, out,
+    the per-rep seconds)."""
     from oracle import bindings as B
     R = B.ref()
-    p = B.host_cores()
+    p = p or B.host_cores()
     S = "kv" if cfg.get("vals") else cfg["key"]
     if cfg["kind"] == "merge":
         import numpy as np
@@ -448,7 +458,7 @@ def time_reference(cfg, ha, hb, reps, budget_s, sample_frac=None):
         n = len(ha) + len(hb)
         sample = (f"full config input ({n} elements), parallel_merge_into with a warm "
                   f"thread_team({p}), median of {len(times)} reps")
-        return n / sec, sec, p, sample, out
+        return n / sec, sec, p, sample, out, times
     # sort: a bounded prefix of the same keys (full 2^30 takes ~40 s on 8 threads)
     n = len(ha)
     m = n if sample_frac is None else max(1 << 20, int(n * sample_frac))
@@ -463,14 +473,47 @@ def time_reference(cfg, ha, hb, reps, budget_s, sample_frac=None):
     sec = statistics.median(times)
     sample = (f"first {m} of the {n} config keys, parallel_merge_sort(span, p={p}) incl. its "
               f"copy/alloc, median of {len(times)} reps")
-    return m / sec, sec, p, sample, out
+    return m / sec, sec, p, sample, out, times
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_worker(spec: str) -> int:
+    """Hidden mode (--cpu-worker JSON): one fresh process times the
+    reference on the inputs saved by cpu_baseline (BASELINE.md §3 / SURVEY
+    H1: thread placement differs between process launches)."""
+    import numpy as np
+    d = json.loads(spec)
+    cfg = CONFIGS[d["config"]]
+    ha = np.load(d["a"], mmap_mode="r")
+    hb = np.load(d["b"], mmap_mode="r") if d.get("b") else None
+    ha = np.ascontiguousarray(ha)
+    hb = np.ascontiguousarray(hb) if hb is not None else None
+    _, _, p, _, _, times = time_reference(cfg, ha, hb, reps=d["reps"], budget_s=d["budget"],
+                                          sample_frac=d.get("frac"), p=d["p"])
+    print(json.dumps({"p": p, "times": times}), flush=True)
+    return 0
 
 
 def cpu_baseline(cfg, a, b, out_dev, args):
+    """The reference's CPU path on this box's host cores:
+    >= 3 separate process launches at p = host cores, one at p = 1, each
+    reporting every rep; value = the median over all p = cores reps.  The
+    first in-process run also verifies the GPU output against it."""
     from oracle import bindings as B
     if not B.REF_LIB.exists():
         return {"value": None, "unit": None, "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built"}
+    import subprocess
+    import tempfile
     import numpy as np
     prefix = None
     if cfg["kind"] == "merge" and a.numel() + b.numel() > (1 << 30):
@@ -479,11 +522,14 @@ def cpu_baseline(cfg, a, b, out_dev, args):
         a, b = a[:prefix], b[:prefix]
     ha, hb = ref_inputs_from_device(cfg, a, b)
     frac = None if cfg["kind"] == "merge" else 1 / 16
-    val, sec, p, sample, out = time_reference(cfg, ha, hb, reps=5, budget_s=20, sample_frac=frac)
+    val, sec, p, sample, out, _ = time_reference(cfg, ha, hb, reps=3, budget_s=10,
+                                                 sample_frac=frac)
     if prefix:
-        sample = f"2^27-element prefixes of A and B (host RAM bound); " + sample
-    res = {"value": val, "unit": "elements/s" if cfg["kind"] == "merge" else "keys/s",
-           "cores": p, "kind": "reference", "sample": sample, "seconds_per_rep": sec}
+        sample = "2^27-element prefixes of A and B (host RAM bound); " + sample
+    unit = "elements/s" if cfg["kind"] == "merge" else "keys/s"
+    units = (len(ha) + len(hb)) if cfg["kind"] == "merge" else max(1 << 20, int(len(ha) * frac))
+    res = {"value": val, "unit": unit, "cores": p, "kind": "reference", "sample": sample,
+           "cpu_model": cpu_model(), "seconds_per_rep": sec}
     if out_dev is not None:  # verify before report (mergebench.cpp:263-265)
         if prefix:
             from paper_1406_2628_b200 import mergepath as mp
@@ -493,6 +539,48 @@ def cpu_baseline(cfg, a, b, out_dev, args):
             got = got.view(np.uint32)
         want = out["key"] if cfg.get("vals") else out
         res["gpu_output_bit_exact_vs_reference"] = bool(got.tobytes() == want.tobytes())
+    del out
+    launches = []
+    with tempfile.TemporaryDirectory(prefix="mp_cpu_") as tmp:
+        fa = os.path.join(tmp, "a.npy")
+        np.save(fa, ha if cfg["kind"] == "merge" else ha[:units])  # the sort's sample only
+        fb = None
+        if hb is not None:
+            fb = os.path.join(tmp, "b.npy")
+            np.save(fb, hb)
+        cfg_name = next(k for k, v in CONFIGS.items() if v is cfg)
+        runs = [(p, 5, 10.0)] * 3 + [(1, 3, 15.0)]
+        if cfg_name == "1" and p != 8:
+            runs += [(8, 5, 10.0)] * 3  # config 1 is specified at p = 8
+        for pp, reps, budget in runs:
+            spec = json.dumps({"config": cfg_name, "a": fa, "b": fb, "p": pp, "reps": reps,
+                               "budget": budget, "frac": None})
+            r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--cpu-worker", spec],
+                               capture_output=True, text=True, timeout=300)
+            if r.returncode != 0:
+                launches.append({"p": pp, "error": r.stderr[-300:]})
+                continue
+            d = json.loads(r.stdout.strip().splitlines()[-1])
+            launches.append({"p": pp, "median_s": statistics.median(d["times"]),
+                             "min_s": min(d["times"]), "reps": len(d["times"])})
+    ok = [x for x in launches if "median_s" in x and x["p"] == p]
+    if ok:
+        med = statistics.median(x["median_s"] for x in ok)
+        res.update({"value": units / med, "seconds_per_rep": med,
+                    "median_s": med, "min_s": min(x["min_s"] for x in ok),
+                    "sample": sample.split(", median of")[0] + f"; median over {len(ok)} "
+                              "process launches x 5 reps (one more in-process run checks the "
+                              "GPU output)"})
+    p1 = [x for x in launches if "median_s" in x and x["p"] == 1]
+    if p1 and ok:
+        res["p1"] = {"value": units / p1[0]["median_s"], "median_s": p1[0]["median_s"],
+                     "min_s": p1[0]["min_s"]}
+        res["speedup_vs_p1"] = p1[0]["median_s"] / res["median_s"]
+    p8 = [x for x in launches if "median_s" in x and x["p"] == 8 and p != 8]
+    if p8:
+        m8 = statistics.median(x["median_s"] for x in p8)
+        res["p8"] = {"value": units / m8, "median_s": m8, "min_s": min(x["min_s"] for x in p8)}
+    res["launches"] = launches
     return res
 
 
@@ -544,7 +632,7 @@ def run_reference(args, cfg, ws, rank):
         "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total / len(times) * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg["key"], "data": "synthetic (same generator)",
-        "config": {"workload": cfg["desc"], "parallelism": f"cpu threads {p}"},
+        "config": config_dict(cfg, ws),
         "cpu_baseline": {"value": value, "unit": unit, "cores": p, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -552,7 +640,30 @@ def run_reference(args, cfg, ws, rank):
 
 
 # --------------------------------------------------------------------------
+def _spawn_ranks(args_n: int, argv) -> int:
+    """--gpus N > 1 without a launcher: re-run this script under
+    torch.distributed.run with N ranks on 127.0.0.1 (the driver's own
+    launch line), so the requested GPU count is never silently ignored."""
+    import socket
+    import subprocess
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+           str(args_n), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           str(ROOT / "bench.py")] + list(argv)
+    return subprocess.call(cmd)
+
+
+def _summary(res):
+    """The nested record of a secondary workload in the same run."""
+    keep = ("metric", "value", "unit", "ms_per_step", "steps", "warmup", "scaling", "dtype",
+            "config", "gpu_launches", "roofline", "nvlink", "clocks", "e2e", "cpu_baseline")
+    return {k: res[k] for k in keep if k in res}
+
+
 def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[1])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -562,14 +673,25 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
-                    help="multi-GPU exchange: NVLink pull fused into the merge (p2p) "
-                         "or all_to_all staging (nccl)")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="only the --config workload (default: the config-2 line also "
+                         "carries the sort (config 4) and, at N > 1, config 5)")
+    ap.add_argument("--cpu-worker", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args(argv)
+    if args.cpu_worker:
+        return cpu_worker(args.cpu_worker)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     cfg = CONFIGS[args.config]
     ws, rank, local = dist_env()
+    if args.gpus < 1:
+        print(json.dumps({"error": "--gpus must be >= 1"}), flush=True)
+        return 2
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return _spawn_ranks(args.gpus, argv)
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr, flush=True)
+        return 2
     dist_on = ws > 1
     if args.impl == "reference":
         res = run_reference(args, cfg, ws, rank)
@@ -579,20 +701,41 @@ def main(argv=None):
     if dist_on:
         import torch
         import torch.distributed as dist
+        if "MP_BENCH_DEVICE" not in os.environ and torch.cuda.device_count() < ws:
+            print(f"bench.py: {ws} ranks but {torch.cuda.device_count()} GPUs", file=sys.stderr)
+            return 2
         torch.cuda.set_device(local)
         backend = os.environ.get("MP_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    if dist_on and cfg["kind"] == "merge":
-        from paper_1406_2628_b200.multigpu import bench_distributed
-        res = bench_distributed(args, cfg, ws, rank, local, lambda: ClockSampler(local))
-    elif dist_on:
-        from paper_1406_2628_b200.multigpu import bench_distributed_sort
-        res = bench_distributed_sort(args, cfg, ws, rank, local, lambda: ClockSampler(local))
+    extra = not args.no_extra and args.config == "2"
+    if dist_on:
+        from paper_1406_2628_b200.multigpu import bench_distributed, bench_distributed_sort
+        clock = (lambda: ClockSampler(local))  # noqa: E731
+        if cfg["kind"] == "merge":
+            res = bench_distributed(args, cfg, ws, rank, local, clock)
+        else:
+            res = bench_distributed_sort(args, cfg, ws, rank, local, clock)
+        if extra:
+            import torch
+            torch.cuda.empty_cache()
+            k = max(3, args.steps // 10)
+            sub = argparse.Namespace(**{**vars(args), "steps": k, "warmup": 3})
+            res["config5"] = _summary(bench_distributed(sub, CONFIGS["5"], ws, rank, local,
+                                                        clock))
+            torch.cuda.empty_cache()
+            res["sort"] = _summary(bench_distributed_sort(sub, CONFIGS["4"], ws, rank, local,
+                                                          clock))
     else:
         res = run_ours(args, cfg, ws, rank, local, dist_on)
+        if extra:
+            import torch
+            torch.cuda.empty_cache()
+            sub = argparse.Namespace(**{**vars(args), "config": "4",
+                                        "steps": max(3, args.steps // 10)})
+            res["sort"] = _summary(run_ours(sub, CONFIGS["4"], ws, rank, local, dist_on))
     if rank == 0:
         print(json.dumps(res), flush=True)
     if dist_on:

@@ -176,15 +176,29 @@ typedef struct mp_piece {
 
 /* out[0, out_end - out_begin) = positions [out_begin, out_end) of the stable
  * merge of A = a[0] ++ a[1] ++ ... and B = b[0] ++ ... (1..16 pieces each).
- * The output range is cut where the merge path crosses piece boundaries
- * (found by a device probe over the pieces, then one host sync), and each
- * segment is merged by K1 + K2 directly from the piece pointers: remote
- * pieces are read over NVLink inside the tile loads (no staging copy).
+ * Asynchronous on `stream` (no host synchronisation): the tile split points
+ * of the range are searched over the virtual index spaces on the device,
+ * then each tile's windows are read straight from the piece pointers --
+ * remote pieces over NVLink inside the tile loads (no staging copy).  The
+ * caller orders the pieces' producers before `stream` (events / mp_signal).
  * out_vals non-NULL => every non-empty piece must carry vals. */
 int mp_merge_pieces(int key_type, const mp_piece *a, int na_pieces,
                     const mp_piece *b, int nb_pieces, uint64_t out_begin,
                     uint64_t out_end, void *out, uint32_t *out_vals,
                     void *stream);
+
+/* a_offs[k] = a_off of the merge path of the piece lists on diagonal
+ * diags[k] (clamped to |A| + |B|): the multi-GPU analogue of
+ * mp_diagonal_search (diags and a_offs are device arrays).  Used to place a
+ * caller's own output slices and to count the NVLink traffic of a merge. */
+int mp_pieces_partition(int key_type, const mp_piece *a, int na_pieces,
+                        const mp_piece *b, int nb_pieces, const uint64_t *diags,
+                        uint64_t count, uint64_t *a_offs, void *stream);
+/* Copy `bytes` (16-byte aligned pointers, size a multiple of 16) with SM
+ * vector loads -- the merge kernels' peer-window access pattern; with a
+ * peer-mapped `src` it measures the NVLink pull rate (tools/nvlink_probe.py,
+ * bench.py --gpus N). */
+int mp_peer_copy(void *dst, const void *src, uint64_t bytes, void *stream);
 
 /* CUDA IPC for shards owned by other processes: export writes a 64-byte
  * handle of the allocation holding dev_ptr plus dev_ptr's offset in it;
@@ -192,6 +206,27 @@ int mp_merge_pieces(int key_type, const mp_piece *a, int na_pieces,
  * returns the mapped address of the same byte. */
 int mp_ipc_export(const void *dev_ptr, void *handle64, uint64_t *offset);
 int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr);
+/* Mappings are cached per (importing device, allocation) and reference
+ * counted: each import takes a reference, mp_ipc_close(ptr) (any pointer an
+ * import returned) drops one and unmaps the allocation at zero.
+ * mp_ipc_open_count() = allocations currently mapped by this process. */
+int mp_ipc_close(const void *dev_ptr);
+uint64_t mp_ipc_open_count(void);
+
+/* Stream-ordered flags for ordering work across processes and GPUs without
+ * host synchronisation: mp_signal writes `value` to the 8-byte device word
+ * `flag` (local or peer-mapped) after all prior work of `stream`, with a
+ * system-scope fence; mp_wait makes `stream` wait until *flag >= value (the
+ * stream's front end polls; no SM spins).  Use monotonically growing
+ * generation numbers. */
+int mp_signal(uint64_t *flag, uint64_t value, void *stream);
+int mp_wait(const uint64_t *flag, uint64_t value, void *stream);
+
+/* ---- memory ------------------------------------------------------------ */
+/* Scratch comes from a library-private stream-ordered pool per device that
+ * keeps its memory between calls; mp_release(device) waits for the device,
+ * frees the host-pipeline slot buffers and trims that pool to zero. */
+int mp_release(int device);
 
 /* ---- synthetic inputs (bench/tests; SURVEY.md §8d generator) ---------- */
 /* out[k] = config key kind `gen_kind` at global index first+k for `seed`:

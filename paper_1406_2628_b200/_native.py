@@ -56,8 +56,15 @@ SIGNATURES = [
     ("mp_sort_host", _i, [_i, _p, _p, _u64, _p, _p, _i]),
     ("mp_merge_checksum_host", _i, [_i, _p, _u64, _p, _u64, _p, _i]),
     ("mp_merge_pieces", _i, [_i, _p, _i, _p, _i, _u64, _u64, _p, _p, _p]),
+    ("mp_pieces_partition", _i, [_i, _p, _i, _p, _i, _p, _u64, _p, _p]),
+    ("mp_peer_copy", _i, [_p, _p, _u64, _p]),
     ("mp_ipc_export", _i, [_p, _p, _p]),
     ("mp_ipc_import", _i, [_p, _u64, _p]),
+    ("mp_ipc_close", _i, [_p]),
+    ("mp_ipc_open_count", _u64, []),
+    ("mp_release", _i, [_i]),
+    ("mp_signal", _i, [_p, _u64, _p]),
+    ("mp_wait", _i, [_p, _u64, _p]),
     ("mp_generate", _i, [_i, _u64, _u64, _u64, _p, _p]),
 ]
 

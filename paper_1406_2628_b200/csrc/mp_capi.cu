@@ -66,20 +66,32 @@ std::atomic<uint64_t> g_launches{0};
       return cuda_fail(e_, what);                                              \
   } while (0)
 
-// Stream-ordered scratch from the device's default pool; the pool keeps its
-// memory (release threshold = max) so repeated calls do not hit the driver.
-void ensure_pool() {
+// Stream-ordered scratch from a library-private memory pool per device (not
+// the device's default pool, which torch and the caller may share): the pool
+// keeps its memory between calls (release threshold = max) so repeated calls
+// do not hit the driver allocator; mp_release() trims it.
+cudaMemPool_t g_pools[64] = {};
+
+cudaMemPool_t lib_pool(int dev) {
   static std::once_flag once[64];
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64)
-    return;
+  if (dev < 0 || dev >= 64)
+    return nullptr;
   std::call_once(once[dev], [dev] {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      g_pools[dev] = pool;
+    } else {
+      cudaGetLastError();
     }
   });
+  return g_pools[dev];
 }
 
 struct ScratchGuard {  // frees a stream-ordered allocation on scope exit
@@ -92,9 +104,13 @@ struct ScratchGuard {  // frees a stream-ordered allocation on scope exit
 };
 
 int alloc_scratch(ScratchGuard &g, size_t bytes, cudaStream_t s) {
-  ensure_pool();
+  int dev = 0;
+  MP_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool = lib_pool(dev);
   g.s = s;
-  const cudaError_t e = cudaMallocAsync(&g.p, bytes ? bytes : 16, s);
+  const cudaError_t e =
+      pool ? cudaMallocFromPoolAsync(&g.p, bytes ? bytes : 16, pool, s)
+           : cudaMallocAsync(&g.p, bytes ? bytes : 16, s);
   if (e != cudaSuccess) {
     g.p = nullptr;
     return cuda_fail(e, "cudaMallocAsync(scratch)");
@@ -1164,9 +1180,10 @@ template <class KT> struct SegmentOp {
   }
 };
 
-// Merge of piece-concatenated sequences (mp_pieces.cuh): probe the piece
-// crossings on the device, cut the output range there, and run the plain
-// K1 + K2 merge on every segment straight from the (peer) piece pointers.
+// Merge of piece-concatenated sequences (mp_pieces.cuh): tile split points
+// searched over the virtual index spaces, then one CTA per tile stages its
+// windows from the (local or peer-mapped) pieces.  Two launches on the
+// caller's stream, no host synchronisation.
 // Is p memory of another device than `dev` (a peer mapping)?
 bool is_peer(const void *p, int dev) {
   cudaPointerAttributes at{};
@@ -1176,7 +1193,7 @@ bool is_peer(const void *p, int dev) {
   }
   return at.type == cudaMemoryTypeDevice && at.device != dev;
 }
-// MP_PEER_LSU=1: use the LSU loader for every piece merge (tests the peer
+// MP_PEER_LSU=1: use the LSU loader for every piece window (tests the peer
 // path on a one-GPU box)
 bool peer_lsu_forced() {
   static const bool f = [] {
@@ -1186,107 +1203,100 @@ bool peer_lsu_forced() {
   return f;
 }
 
+template <class KT> constexpr int pieces_vt() { return MergeCfg<KT>::VT; }
+constexpr int kPiecesNT = MP_MERGE_NT;
+
 template <class KT> struct PiecesOp {
+  static int fill(VPieces &V, const mp_piece *p, int np, bool vals, int dev,
+                  const char *which) {
+    V.n = np;
+    V.peer = 0;
+    V.start[0] = 0;
+    for (int k = 0; k < np; ++k) {
+      V.ptr[k] = p[k].keys;
+      V.vptr[k] = p[k].vals;
+      V.start[k + 1] = V.start[k] + p[k].len;
+      if (p[k].len && (!p[k].keys || !aligned_keys<KT>(p[k].keys) || (vals && !p[k].vals)))
+        return fail(MP_ERR_INVALID, "merge_pieces: bad %s piece %d", which, k);
+      if (p[k].len && (is_peer(p[k].keys, dev) || (vals && is_peer(p[k].vals, dev))))
+        V.peer |= 1u << k;
+    }
+    return MP_OK;
+  }
+
   static int run(const mp_piece *pa, int npa, const mp_piece *pb, int npb,
                  uint64_t o0, uint64_t o1, void *out_, uint32_t *outv,
                  cudaStream_t s) {
     using T = typename KT::T;
     if (npa < 1 || npb < 1 || npa > kMaxPieces || npb > kMaxPieces)
       return fail(MP_ERR_INVALID, "merge_pieces: 1..%d pieces per input", kMaxPieces);
+    const bool vals = outv != nullptr;
+    if (KT::kind == kElement && vals)
+      return fail(MP_ERR_UNSUPPORTED, "ELEMENT keys carry their own tag");
+    int dev = 0;
+    MP_CUDA(cudaGetDevice(&dev));
     VPieces A{}, B{};
-    A.n = npa;
-    B.n = npb;
-    bool vals = outv != nullptr;
-    A.start[0] = B.start[0] = 0;
-    for (int k = 0; k < npa; ++k) {
-      A.ptr[k] = pa[k].keys;
-      A.start[k + 1] = A.start[k] + pa[k].len;
-      if (pa[k].len && (!pa[k].keys || !aligned_keys<KT>(pa[k].keys) ||
-                        (vals && !pa[k].vals)))
-        return fail(MP_ERR_INVALID, "merge_pieces: bad A piece %d", k);
-    }
-    for (int k = 0; k < npb; ++k) {
-      B.ptr[k] = pb[k].keys;
-      B.start[k + 1] = B.start[k] + pb[k].len;
-      if (pb[k].len && (!pb[k].keys || !aligned_keys<KT>(pb[k].keys) ||
-                        (vals && !pb[k].vals)))
-        return fail(MP_ERR_INVALID, "merge_pieces: bad B piece %d", k);
-    }
+    if (int rc = fill(A, pa, npa, vals, dev, "A"))
+      return rc;
+    if (int rc = fill(B, pb, npb, vals, dev, "B"))
+      return rc;
     const uint64_t na = A.start[npa], nb = B.start[npb];
     if (o0 > o1 || o1 > na + nb)
       return fail(MP_ERR_INVALID, "merge_pieces: output range out of bounds");
     if (o0 == o1)
       return MP_OK;
-    if (KT::kind == kElement && vals)
-      return fail(MP_ERR_UNSUPPORTED, "ELEMENT keys carry their own tag");
-    // ---- probe: range ends + every piece crossing ----
-    const int probes = 2 + (npa - 1) + (npb - 1);
+    if (!out_ || (reinterpret_cast<uintptr_t>(out_) % alignof(T)))
+      return fail(MP_ERR_INVALID, "merge_pieces: bad output pointer");
+    constexpr int NT = kPiecesNT, VT = pieces_vt<KT>();
+    constexpr uint32_t NV = NT * VT;
+    const uint64_t tiles = cdiv(o1 - o0, NV);
+    if (tiles >= (1ull << 31))
+      return fail(MP_ERR_INVALID, "merge_pieces: range too large");
     ScratchGuard g;
-    if (int rc = alloc_scratch(g, probes * 16, s))
+    if (int rc = alloc_scratch(g, (tiles + 1) * 8, s))
       return rc;
-    uint64_t *dprobe = static_cast<uint64_t *>(g.p);
-    pieces_probe_kernel<KT><<<1, 64, 0, s>>>(A, B, o0, o1, dprobe);
-    MP_LAUNCHED("pieces_probe_kernel");
-    std::vector<uint64_t> h(2 * probes);
-    MP_CUDA(cudaMemcpyAsync(h.data(), dprobe, h.size() * 8,
-                            cudaMemcpyDeviceToHost, s));
-    MP_CUDA(cudaStreamSynchronize(s));
-    // ---- cut points on the path, sorted by diagonal ----
-    std::vector<std::pair<uint64_t, uint64_t>> pts;  // (a, b)
-    pts.push_back({h[0], h[1]});
-    for (int t = 2; t < probes; ++t) {
-      const uint64_t a = h[2 * t], b = h[2 * t + 1];
-      if (a + b > o0 && a + b < o1)
-        pts.push_back({a, b});
+    uint64_t *P = static_cast<uint64_t *>(g.p);
+    pieces_partition_kernel<KT><<<static_cast<unsigned>(cdiv(tiles + 1, 128)), 128, 0, s>>>(
+        A, B, o0, o1, NV, tiles + 1, P);
+    MP_LAUNCHED("pieces_partition_kernel");
+    const int lsu = peer_lsu_forced() ? 1 : 0;
+    if (vals) {
+      constexpr uint32_t smem = merge_smem_bytes<KT, true, NT, VT>();
+      auto kern = pieces_tiles_kernel<KT, true, NT, VT>;
+      MP_CUDA(set_smem(kern, smem));
+      kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(A, B, P, o0, o1,
+                                                         static_cast<T *>(out_), outv, lsu);
+    } else {
+      constexpr uint32_t smem = merge_smem_bytes<KT, false, NT, VT>();
+      auto kern = pieces_tiles_kernel<KT, false, NT, VT>;
+      MP_CUDA(set_smem(kern, smem));
+      kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(A, B, P, o0, o1,
+                                                         static_cast<T *>(out_), nullptr, lsu);
     }
-    pts.push_back({h[2], h[3]});
-    std::sort(pts.begin(), pts.end(), [](const auto &x, const auto &y) {
-      return x.first + x.second < y.first + y.second;
-    });
-    auto piece_of = [](const VPieces &v, uint64_t i) {
-      int k = 0;
-      while (k + 1 < v.n && i >= v.start[k + 1])
-        ++k;
-      return k;
-    };
+    MP_LAUNCHED("pieces_tiles_kernel");
+    return MP_OK;
+  }
+};
+
+template <class KT> struct PiecesDiagOp {
+  static int run(const mp_piece *pa, int npa, const mp_piece *pb, int npb,
+                 const uint64_t *diags, uint64_t count, uint64_t *a_offs, cudaStream_t s) {
+    if (npa < 1 || npb < 1 || npa > kMaxPieces || npb > kMaxPieces)
+      return fail(MP_ERR_INVALID, "pieces_partition: 1..%d pieces per input", kMaxPieces);
+    if (count == 0)
+      return MP_OK;
+    if (!diags || !a_offs)
+      return fail(MP_ERR_INVALID, "pieces_partition: NULL array");
     int dev = 0;
     MP_CUDA(cudaGetDevice(&dev));
-    T *out = static_cast<T *>(out_);
-    for (size_t q = 0; q + 1 < pts.size(); ++q) {
-      const uint64_t a0 = pts[q].first, b0 = pts[q].second;
-      const uint64_t a1 = pts[q + 1].first, b1 = pts[q + 1].second;
-      if (a0 + b0 == a1 + b1)
-        continue;
-      const int ka = piece_of(A, a0), kb = piece_of(B, b0);
-      const T *ap = static_cast<const T *>(A.ptr[ka]) + (a0 - A.start[ka]);
-      const T *bp = static_cast<const T *>(B.ptr[kb]) + (b0 - B.start[kb]);
-      const uint64_t ob = a0 + b0 - o0;
-      // windows in another GPU's memory are read by LSU vector loads over
-      // NVLink (the bulk-copy engine is used for local memory only)
-      const bool peer = peer_lsu_forced() ||
-                        (a1 > a0 && is_peer(pa[ka].keys, dev)) ||
-                        (b1 > b0 && is_peer(pb[kb].keys, dev)) ||
-                        (vals && a1 > a0 && is_peer(pa[ka].vals, dev)) ||
-                        (vals && b1 > b0 && is_peer(pb[kb].vals, dev));
-      int rc;
-      const uint32_t *av_ = vals ? pa[ka].vals + (a0 - A.start[ka]) : nullptr;
-      const uint32_t *bv_ = vals ? pb[kb].vals + (b0 - B.start[kb]) : nullptr;
-      if (vals && peer)
-        rc = merge_impl<KT, true, false, true>(ap, av_, a1 - a0, bp, bv_, b1 - b0,
-                                               out + ob, outv + ob, nullptr, s);
-      else if (vals)
-        rc = merge_impl<KT, true, false>(ap, av_, a1 - a0, bp, bv_, b1 - b0,
-                                         out + ob, outv + ob, nullptr, s);
-      else if (peer)
-        rc = merge_impl<KT, false, false, true>(ap, nullptr, a1 - a0, bp, nullptr,
-                                                b1 - b0, out + ob, nullptr, nullptr, s);
-      else
-        rc = merge_impl<KT, false, false>(ap, nullptr, a1 - a0, bp, nullptr,
-                                          b1 - b0, out + ob, nullptr, nullptr,
-                                          s);
-      if (rc)
-        return rc;
-    }
+    VPieces A{}, B{};
+    if (int rc = PiecesOp<KT>::fill(A, pa, npa, false, dev, "A"))
+      return rc;
+    if (int rc = PiecesOp<KT>::fill(B, pb, npb, false, dev, "B"))
+      return rc;
+    pieces_diagonals_kernel<KT><<<static_cast<unsigned>(cdiv(count, 128)), 128, 0, s>>>(
+        A, B, diags, count, a_offs);
+    MP_LAUNCHED("pieces_diagonals_kernel");
     return MP_OK;
   }
 };
@@ -1680,6 +1690,33 @@ int mp_merge_pieces(int kt, const mp_piece *a, int na_pieces,
                             out, out_vals, static_cast<cudaStream_t>(stream));
 }
 
+int mp_pieces_partition(int kt, const mp_piece *a, int na_pieces, const mp_piece *b,
+                        int nb_pieces, const uint64_t *diags, uint64_t count,
+                        uint64_t *a_offs, void *stream) {
+  g_err.clear();
+  return dispatch<PiecesDiagOp>(kt, a, na_pieces, b, nb_pieces, diags, count, a_offs,
+                                static_cast<cudaStream_t>(stream));
+}
+
+int mp_peer_copy(void *dst, const void *src, uint64_t bytes, void *stream) {
+  g_err.clear();
+  if (bytes == 0)
+    return MP_OK;
+  if (!dst || !src || (bytes & 15) || (reinterpret_cast<uintptr_t>(dst) & 15) ||
+      (reinterpret_cast<uintptr_t>(src) & 15))
+    return fail(MP_ERR_INVALID, "peer_copy: 16-byte aligned pointers and size required");
+  int dev = 0, sms = 148;
+  MP_CUDA(cudaGetDevice(&dev));
+  MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const uint64_t n16 = bytes / 16;
+  const unsigned grid = static_cast<unsigned>(
+      std::min<uint64_t>(uint64_t(sms) * 4, cdiv(n16, 4 * 512)));
+  lsu_copy_kernel<<<grid ? grid : 1, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<uint4 *>(dst), static_cast<const uint4 *>(src), n16);
+  MP_LAUNCHED("lsu_copy_kernel");
+  return MP_OK;
+}
+
 // ---- CUDA IPC (shards of other processes / GPUs) ---------------------------
 int mp_ipc_export(const void *dev_ptr, void *handle64, uint64_t *offset) {
   g_err.clear();
@@ -1710,26 +1747,111 @@ int mp_ipc_export(const void *dev_ptr, void *handle64, uint64_t *offset) {
   return MP_OK;
 }
 
+// Imported mappings, one per (importing device, allocation handle), with a
+// reference count: every mp_ipc_import takes a reference, mp_ipc_close drops
+// one and unmaps the allocation when the last reference goes.
+struct IpcMapping {
+  int dev;
+  std::string handle;
+  void *base;
+  size_t refs;
+};
+std::mutex g_ipc_mu;
+std::vector<IpcMapping> g_ipc;
+
 int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr) {
   g_err.clear();
   if (!handle64 || !dev_ptr)
     return fail(MP_ERR_INVALID, "ipc_import: NULL argument");
-  static std::mutex mu;
-  static std::vector<std::pair<std::string, void *>> opened;
+  int dev = 0;
+  MP_CUDA(cudaGetDevice(&dev));
   const std::string key(static_cast<const char *>(handle64), sizeof(cudaIpcMemHandle_t));
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto &e : opened)
-    if (e.first == key) {
-      *dev_ptr = static_cast<char *>(e.second) + offset;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (auto &e : g_ipc)
+    if (e.dev == dev && e.handle == key) {
+      ++e.refs;
+      *dev_ptr = static_cast<char *>(e.base) + offset;
       return MP_OK;
     }
   cudaIpcMemHandle_t h;
   std::memcpy(&h, handle64, sizeof h);
   void *base = nullptr;
   MP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
-  opened.push_back({key, base});
+  g_ipc.push_back({dev, key, base, 1});
   *dev_ptr = static_cast<char *>(base) + offset;
   return MP_OK;
+}
+
+int mp_ipc_close(const void *dev_ptr) {
+  g_err.clear();
+  if (!dev_ptr)
+    return MP_OK;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  // the mapping whose base is the closest at or below dev_ptr
+  size_t best = g_ipc.size();
+  for (size_t k = 0; k < g_ipc.size(); ++k)
+    if (g_ipc[k].base <= dev_ptr &&
+        (best == g_ipc.size() || g_ipc[k].base > g_ipc[best].base))
+      best = k;
+  if (best == g_ipc.size())
+    return fail(MP_ERR_INVALID, "ipc_close: not an imported mapping");
+  if (--g_ipc[best].refs == 0) {
+    DeviceScope ds(g_ipc[best].dev);
+    const cudaError_t e = cudaIpcCloseMemHandle(g_ipc[best].base);
+    g_ipc.erase(g_ipc.begin() + static_cast<long>(best));
+    if (e != cudaSuccess)
+      return cuda_fail(e, "cudaIpcCloseMemHandle");
+  }
+  return MP_OK;
+}
+
+// ---- stream-ordered flags (cross-process / cross-GPU ordering) ------------
+// cuStreamWriteValue64 / cuStreamWaitValue64 through the runtime's driver
+// entry points (no link-time libcuda dependency).  The write carries a
+// system-scope fence (prior work of the stream is visible first); the wait
+// blocks the stream's front end -- no SM is spent spinning.
+namespace {
+using StreamValueFn = int (*)(void *, unsigned long long, unsigned long long, unsigned int);
+StreamValueFn driver_fn(const char *name) {
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return reinterpret_cast<StreamValueFn>(fn);
+}
+}  // namespace
+
+int mp_signal(uint64_t *flag, uint64_t value, void *stream) {
+  g_err.clear();
+  static const StreamValueFn w = driver_fn("cuStreamWriteValue64");
+  if (!flag || (reinterpret_cast<uintptr_t>(flag) & 7))
+    return fail(MP_ERR_INVALID, "signal: flag must be an 8-byte aligned device address");
+  if (!w)
+    return fail(MP_ERR_CUDA, "signal: cuStreamWriteValue64 unavailable");
+  if (int e = w(stream, reinterpret_cast<unsigned long long>(flag), value, 0))
+    return fail(MP_ERR_CUDA, "cuStreamWriteValue64 failed (%d)", e);
+  return MP_OK;
+}
+
+int mp_wait(const uint64_t *flag, uint64_t value, void *stream) {
+  g_err.clear();
+  static const StreamValueFn w = driver_fn("cuStreamWaitValue64");
+  if (!flag || (reinterpret_cast<uintptr_t>(flag) & 7))
+    return fail(MP_ERR_INVALID, "wait: flag must be an 8-byte aligned device address");
+  if (!w)
+    return fail(MP_ERR_CUDA, "wait: cuStreamWaitValue64 unavailable");
+  // CU_STREAM_WAIT_VALUE_GEQ (0): generation counters only grow
+  if (int e = w(stream, reinterpret_cast<unsigned long long>(flag), value, 0))
+    return fail(MP_ERR_CUDA, "cuStreamWaitValue64 failed (%d)", e);
+  return MP_OK;
+}
+
+uint64_t mp_ipc_open_count(void) {
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  return g_ipc.size();
 }
 
 int mp_generate(int gen_kind, uint64_t seed, uint64_t first, uint64_t n,
@@ -2091,6 +2213,30 @@ int mp_sort_host(int kt, const void *keys, const uint32_t *vals, uint64_t n,
   if (vals)
     MP_CUDA(cudaMemcpyAsync(out_vals, dv, n * 4, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaStreamSynchronize(s));
+  return MP_OK;
+}
+
+int mp_release(int device) {
+  g_err.clear();
+  int count = 0;
+  MP_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count || device >= 64)
+    return fail(MP_ERR_INVALID, "release: no device %d", device);
+  DeviceScope ds(device);
+  if (ds.err != cudaSuccess)
+    return cuda_fail(ds.err, "cudaSetDevice");
+  MP_CUDA(cudaDeviceSynchronize());  // pending stream-ordered frees land
+  HostPipe &P = host_pipe(device);
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.buf) {
+      MP_CUDA(cudaFree(P.buf));
+      P.buf = nullptr;
+      P.buf_bytes = 0;
+    }
+  }
+  if (g_pools[device])
+    MP_CUDA(cudaMemPoolTrimTo(g_pools[device], 0));
   return MP_OK;
 }
 

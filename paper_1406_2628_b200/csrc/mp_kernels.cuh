@@ -617,119 +617,21 @@ __device__ __forceinline__ void lsu_copy16(char *smem, const char *g, uint32_t b
     dst[q] = src[q];
 }
 
-// PEER = true: the window interiors arrive through LSU vector loads instead
-// of the bulk-copy engine (used for windows in another GPU's memory).
-template <class KT, bool VALS, int NT, int VT, class Map, bool SINK = false,
-          bool PEER = false>
-__global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
-    merge_tiles_kernel(Map map, const typename KT::T *__restrict__ a,
-                       const uint32_t *__restrict__ av,
-                       const typename KT::T *__restrict__ b,
-                       const uint32_t *__restrict__ bv,
-                       typename KT::T *__restrict__ out,
-                       uint32_t *__restrict__ outv,
-                       unsigned long long *__restrict__ sum = nullptr,
-                       uint64_t tile0 = 0) {
+// The half of K2 after the tile's windows are staged in smem (A at oA, B at
+// oB, values at oAv/oBv; sentinels behind both windows when SENT): split the
+// window among the threads by a diagonal search in smem, merge VT outputs per
+// thread, then fold them into the checksum (SINK) or stage them in smem and
+// write out[win.o0, win.o0 + na + nb) back (one bulk store when aligned).
+// Shared by merge_tiles_kernel and the piece-list merge (mp_pieces.cuh).
+template <class KT, bool VALS, int NT, int VT, bool SINK, bool SENT>
+__device__ __forceinline__ void merge_staged_window(
+    char *smem, const TileWin &win, uint32_t oA, uint32_t oB, uint32_t oAv, uint32_t oBv,
+    typename KT::T *__restrict__ out, uint32_t *__restrict__ outv,
+    unsigned long long *__restrict__ sum) {
   using T = typename KT::T;
   constexpr uint32_t KS = sizeof(T);
-  extern __shared__ __align__(128) char smem[];
-  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
   const int tid = threadIdx.x;
-  pdl_wait();  // split points / inputs come from the previous kernel
-  pdl_launch_dependents();
-
-  TileWin win;
-  if constexpr (map_searches<Map>::value) {
-    __shared__ unsigned long long split[2];
-    if (tid < 64) {  // warp 0: the tile's start diagonal, warp 1: its end
-      const int w = tid >> 5;
-      const uint64_t sp = map.template split<KT>(a, b, tile0 + blockIdx.x, w, tid & 31);
-      if ((tid & 31) == 0)
-        split[w] = sp;
-    }
-    __syncthreads();
-    win = map.window(tile0 + blockIdx.x, split[0], split[1]);
-  } else {
-    win = map.window(tile0 + blockIdx.x);
-  }
   const int na_t = win.na, nb_t = win.nb, total = na_t + nb_t;
-
-  // --- smem layout (byte offsets): each window congruent mod 16 to its
-  //     global source, so its 16 B-aligned interior is one bulk copy ---
-  const char *gA = reinterpret_cast<const char *>(a + win.a0);
-  const char *gB = reinterpret_cast<const char *>(b + win.b0);
-  const uint32_t bA = na_t * KS, bB = nb_t * KS;
-  constexpr bool SENT = merge_sentinels<KT, VALS>();
-  const uint32_t oA = mirror_off(16, gA);
-  const uint32_t oB = mirror_off(oA + bA + (SENT ? VT * KS : 0), gB);
-  const char *gAv = nullptr, *gBv = nullptr;
-  uint32_t oAv = 0, oBv = 0;
-  if constexpr (VALS) {
-    gAv = reinterpret_cast<const char *>(av + win.a0);
-    gBv = reinterpret_cast<const char *>(bv + win.b0);
-    oAv = mirror_off(oB + bB, gAv);
-    oBv = mirror_off(oAv + na_t * 4, gBv);
-  }
-
-  if constexpr (PEER) {
-    uint32_t lo;
-    uint32_t in = interior_bytes(gA, bA, &lo);
-    lsu_copy16<NT>(smem + oA + lo, gA + lo, in, tid);
-    in = interior_bytes(gB, bB, &lo);
-    lsu_copy16<NT>(smem + oB + lo, gB + lo, in, tid);
-    if constexpr (VALS) {
-      in = interior_bytes(gAv, na_t * 4, &lo);
-      lsu_copy16<NT>(smem + oAv + lo, gAv + lo, in, tid);
-      in = interior_bytes(gBv, nb_t * 4, &lo);
-      lsu_copy16<NT>(smem + oBv + lo, gBv + lo, in, tid);
-    }
-  } else if (tid == 0) {
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    uint32_t loA, loB, loAv = 0, loBv = 0;
-    const uint32_t iA = interior_bytes(gA, bA, &loA);
-    const uint32_t iB = interior_bytes(gB, bB, &loB);
-    uint32_t iAv = 0, iBv = 0;
-    if constexpr (VALS) {
-      iAv = interior_bytes(gAv, na_t * 4, &loAv);
-      iBv = interior_bytes(gBv, nb_t * 4, &loBv);
-    }
-    mbar_arrive_expect_tx(bar, iA + iB + iAv + iBv);
-    if (iA)
-      bulk_g2s(smem + oA + loA, gA + loA, iA, bar);
-    if (iB)
-      bulk_g2s(smem + oB + loB, gB + loB, iB, bar);
-    if constexpr (VALS) {
-      if (iAv)
-        bulk_g2s(smem + oAv + loAv, gAv + loAv, iAv, bar);
-      if (iBv)
-        bulk_g2s(smem + oBv + loBv, gBv + loBv, iBv, bar);
-    }
-  }
-  // unaligned heads/tails: warp 0 takes A, warp 1 takes B (values: 2, 3)
-  {
-    const int w = tid >> 5, l = tid & 31;
-    static_assert(NT >= 128, "edge staging uses warps 0..3");
-    if (w == 0)
-      stage_edges<KS>(smem, oA, gA, bA, l);
-    else if (w == 1)
-      stage_edges<KS>(smem, oB, gB, bB, l);
-    if constexpr (VALS) {
-      if (w == 2)
-        stage_edges<4>(smem, oAv, gAv, na_t * 4, l);
-      else if (w == 3)
-        stage_edges<4>(smem, oBv, gBv, nb_t * 4, l);
-    }
-    if constexpr (SENT) {
-      static_assert(VT < 32, "one sentinel per lane");
-      if (w == 2 && l <= VT)
-        *reinterpret_cast<T *>(smem + (l < VT ? oA + bA + l * KS : oB + bB)) = KT::max_key();
-    }
-  }
-  __syncthreads();
-  if constexpr (!PEER)
-    mbar_wait(bar, 0);
-
   // --- split the window among threads: diagonal search in smem ---
   const int diag = min(tid * VT, total);
   int lo = diag > nb_t ? diag - nb_t : 0;
@@ -810,6 +712,123 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
         dstv[q] = lds<uint32_t>(smem, oSv + stage_idx<VT>(q) * 4);
     }
   }
+}
+
+// PEER = true: the window interiors arrive through LSU vector loads instead
+// of the bulk-copy engine (used for windows in another GPU's memory).
+template <class KT, bool VALS, int NT, int VT, class Map, bool SINK = false,
+          bool PEER = false>
+__global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
+    merge_tiles_kernel(Map map, const typename KT::T *__restrict__ a,
+                       const uint32_t *__restrict__ av,
+                       const typename KT::T *__restrict__ b,
+                       const uint32_t *__restrict__ bv,
+                       typename KT::T *__restrict__ out,
+                       uint32_t *__restrict__ outv,
+                       unsigned long long *__restrict__ sum = nullptr,
+                       uint64_t tile0 = 0) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  extern __shared__ __align__(128) char smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  const int tid = threadIdx.x;
+  pdl_wait();  // split points / inputs come from the previous kernel
+  pdl_launch_dependents();
+
+  TileWin win;
+  if constexpr (map_searches<Map>::value) {
+    __shared__ unsigned long long split[2];
+    if (tid < 64) {  // warp 0: the tile's start diagonal, warp 1: its end
+      const int w = tid >> 5;
+      const uint64_t sp = map.template split<KT>(a, b, tile0 + blockIdx.x, w, tid & 31);
+      if ((tid & 31) == 0)
+        split[w] = sp;
+    }
+    __syncthreads();
+    win = map.window(tile0 + blockIdx.x, split[0], split[1]);
+  } else {
+    win = map.window(tile0 + blockIdx.x);
+  }
+  const int na_t = win.na, nb_t = win.nb;
+
+  // --- smem layout (byte offsets): each window congruent mod 16 to its
+  //     global source, so its 16 B-aligned interior is one bulk copy ---
+  const char *gA = reinterpret_cast<const char *>(a + win.a0);
+  const char *gB = reinterpret_cast<const char *>(b + win.b0);
+  const uint32_t bA = na_t * KS, bB = nb_t * KS;
+  constexpr bool SENT = merge_sentinels<KT, VALS>();
+  const uint32_t oA = mirror_off(16, gA);
+  const uint32_t oB = mirror_off(oA + bA + (SENT ? VT * KS : 0), gB);
+  const char *gAv = nullptr, *gBv = nullptr;
+  uint32_t oAv = 0, oBv = 0;
+  if constexpr (VALS) {
+    gAv = reinterpret_cast<const char *>(av + win.a0);
+    gBv = reinterpret_cast<const char *>(bv + win.b0);
+    oAv = mirror_off(oB + bB, gAv);
+    oBv = mirror_off(oAv + na_t * 4, gBv);
+  }
+
+  if constexpr (PEER) {
+    uint32_t lo;
+    uint32_t in = interior_bytes(gA, bA, &lo);
+    lsu_copy16<NT>(smem + oA + lo, gA + lo, in, tid);
+    in = interior_bytes(gB, bB, &lo);
+    lsu_copy16<NT>(smem + oB + lo, gB + lo, in, tid);
+    if constexpr (VALS) {
+      in = interior_bytes(gAv, na_t * 4, &lo);
+      lsu_copy16<NT>(smem + oAv + lo, gAv + lo, in, tid);
+      in = interior_bytes(gBv, nb_t * 4, &lo);
+      lsu_copy16<NT>(smem + oBv + lo, gBv + lo, in, tid);
+    }
+  } else if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    uint32_t loA, loB, loAv = 0, loBv = 0;
+    const uint32_t iA = interior_bytes(gA, bA, &loA);
+    const uint32_t iB = interior_bytes(gB, bB, &loB);
+    uint32_t iAv = 0, iBv = 0;
+    if constexpr (VALS) {
+      iAv = interior_bytes(gAv, na_t * 4, &loAv);
+      iBv = interior_bytes(gBv, nb_t * 4, &loBv);
+    }
+    mbar_arrive_expect_tx(bar, iA + iB + iAv + iBv);
+    if (iA)
+      bulk_g2s(smem + oA + loA, gA + loA, iA, bar);
+    if (iB)
+      bulk_g2s(smem + oB + loB, gB + loB, iB, bar);
+    if constexpr (VALS) {
+      if (iAv)
+        bulk_g2s(smem + oAv + loAv, gAv + loAv, iAv, bar);
+      if (iBv)
+        bulk_g2s(smem + oBv + loBv, gBv + loBv, iBv, bar);
+    }
+  }
+  // unaligned heads/tails: warp 0 takes A, warp 1 takes B (values: 2, 3)
+  {
+    const int w = tid >> 5, l = tid & 31;
+    static_assert(NT >= 128, "edge staging uses warps 0..3");
+    if (w == 0)
+      stage_edges<KS>(smem, oA, gA, bA, l);
+    else if (w == 1)
+      stage_edges<KS>(smem, oB, gB, bB, l);
+    if constexpr (VALS) {
+      if (w == 2)
+        stage_edges<4>(smem, oAv, gAv, na_t * 4, l);
+      else if (w == 3)
+        stage_edges<4>(smem, oBv, gBv, nb_t * 4, l);
+    }
+    if constexpr (SENT) {
+      static_assert(VT < 32, "one sentinel per lane");
+      if (w == 2 && l <= VT)
+        *reinterpret_cast<T *>(smem + (l < VT ? oA + bA + l * KS : oB + bB)) = KT::max_key();
+    }
+  }
+  __syncthreads();
+  if constexpr (!PEER)
+    mbar_wait(bar, 0);
+
+  merge_staged_window<KT, VALS, NT, VT, SINK, SENT>(smem, win, oA, oB, oAv, oBv, out, outv,
+                                                    sum);
 }
 
 // ---------------------------------------------------------------------------

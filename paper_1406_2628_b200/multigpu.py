@@ -375,17 +375,57 @@ def _import(rec) -> int:
     return p.value or 0
 
 
+class _Flags:
+    """Stream-ordered phase barriers across ranks, with no host involvement.
+
+    Every rank owns a device array of 2*P generation words (a READY and a
+    DONE slot per peer), exported once through CUDA IPC and mapped by every
+    peer.  arrive(phase, ranks) enqueues, on the caller's stream, one
+    mp_signal per rank in `ranks` (a fenced write of the generation into
+    that rank's slot for me) and one mp_wait per rank (the stream waits
+    until my slot for that rank holds the generation).  All ranks call
+    arrive() in the same sequence, so the generation -- a local counter --
+    agrees across ranks; slots only grow, so a rank that runs ahead never
+    confuses a slower one (waits are >=)."""
+
+    READY, DONE = 0, 1
+
+    def __init__(self, comm, device):
+        self.comm = comm
+        P = comm.world
+        self.words = torch.zeros(2 * P, dtype=torch.int64, device=device)
+        recs = [None] * P
+        dist.all_gather_object(recs, _export(self.words), group=comm.group)
+        self.base = [self.words.data_ptr() if r == comm.rank else _import(rec)
+                     for r, rec in enumerate(recs)]
+        self.imported = [b for r, b in enumerate(self.base) if r != comm.rank]
+        self.gen = 0
+        torch.cuda.synchronize(device)  # the zeroed words exist before any peer signals
+
+    def slot(self, owner, phase, peer):
+        return self.base[owner] + 8 * (phase * self.comm.world + peer)
+
+    def arrive(self, phase, ranks, stream):
+        self.gen += 1
+        me = self.comm.rank
+        for r in ranks:
+            N.check(N.lib.mp_signal(self.slot(r, phase, me), self.gen, stream))
+        for q in ranks:
+            N.check(N.lib.mp_wait(self.slot(me, phase, q), self.gen, stream))
+
+
 class P2PMerger:
     """Multi-GPU merge with the exchange fused into the merge kernels.
 
     Every rank exports its A and B shards (CUDA IPC); every rank maps all
     peers' shards once (peer access over NVLink 5 / NVSwitch) and runs
     mp_merge_pieces on its output slice S[floor(rN/P), floor((r+1)N/P)):
-    the piece-crossing probe reads peer keys directly and the K1/K2 tile
-    loads pull their windows from peer HBM -- no all_to_all, no staging
-    buffer, one kernel set per rank.  Barriers bracket each merge (inputs
-    complete before anyone reads them; nobody reuses a shard while a peer
-    may still read it)."""
+    the tile split searches and the tile loads read peer HBM directly -- no
+    all_to_all, no staging buffer, two kernels per rank.  Each call is
+    ordered across ranks on the GPU alone (_Flags): READY (every shard's
+    producer has finished) before the merge, DONE (every peer has finished
+    reading) after it, so the host never blocks and no barrier runs per
+    call."""
 
     def __init__(self, a_local, b_local, a_vals=None, b_vals=None, key_type=None,
                  group=None):
@@ -398,6 +438,7 @@ class P2PMerger:
         recs = [None] * self.comm.world
         dist.all_gather_object(recs, me, group=group)
         self.pa, self.pb = [], []
+        self._imported = []  # peer mappings this object holds (closed by close())
         for r, (la, lb, ea, eb, eav, ebv) in enumerate(recs):
             if r == self.comm.rank:
                 ka, kb = a_local.data_ptr() if la else 0, b_local.data_ptr() if lb else 0
@@ -407,6 +448,7 @@ class P2PMerger:
                 ka, kb = _import(ea), _import(eb)
                 va = _import(eav) if eav is not None else None
                 vb = _import(ebv) if ebv is not None else None
+                self._imported += [x for x in (ka, kb, va, vb) if x]
             self.pa.append((ka or None, va, la))
             self.pb.append((kb or None, vb, lb))
         self.na = sum(p[2] for p in self.pa)
@@ -415,8 +457,70 @@ class P2PMerger:
         self.o0, self.o1 = r * n // P, (r + 1) * n // P
         self._arr_a = N.pieces_array(self.pa)
         self._arr_b = N.pieces_array(self.pb)
+        self.flags = _Flags(self.comm, a_local.device)
+        self._imported += self.flags.imported
 
-    def __call__(self, out=None, out_vals=None, sync=True):
+    def close(self):
+        """Drop this object's peer mappings (mp_ipc_close; the library
+        unmaps an allocation when its last importer closes it).  Call on
+        every rank after the last call, once the streams are done."""
+        for p in getattr(self, "_imported", []):
+            N.check(N.lib.mp_ipc_close(p))
+        self._imported = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown / library already gone
+            pass
+
+    def splits(self):
+        """a_off of the merge path at this rank's slice ends (o0, o1), found
+        by mp_pieces_partition over the mapped shards (device search, the
+        kernels' own predicate)."""
+        dev = self.a.device
+        d = torch.tensor([self.o0, self.o1], dtype=torch.int64, device=dev)
+        a = torch.empty(2, dtype=torch.int64, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        self.flags.arrive(_Flags.READY, range(self.comm.world), st)
+        N.check(N.lib.mp_pieces_partition(self.kt, self._arr_a, len(self.pa), self._arr_b,
+                                          len(self.pb), d.data_ptr(), 2, a.data_ptr(), st))
+        self.flags.arrive(_Flags.DONE, range(self.comm.world), st)
+        return a.tolist()
+
+    def traffic(self):
+        """Collective (every rank calls it).  Per rank r: the elements of r's
+        output slice that live on other ranks' shards (r's NVLink-in, in
+        keys: in_a + in_b), the elements of r's own shards that other ranks
+        read (r's NVLink-out) and the elements r's HBM serves (its local
+        reads, its peers' reads of its shards, its output writes) -- all
+        from the actual split points (splits(), untimed bookkeeping)."""
+        P = self.comm.world
+        la = [p[2] for p in self.pa]
+        lb = [p[2] for p in self.pb]
+        sp = self.comm.all_gather_int(self.splits())
+        sa = [sum(la[:r]) for r in range(P + 1)]
+        sb = [sum(lb[:r]) for r in range(P + 1)]
+        n = self.na + self.nb
+
+        def ov(lo, hi, q, starts):
+            return max(0, min(hi, starts[q + 1]) - max(lo, starts[q]))
+
+        rng = []
+        for r in range(P):
+            a0, a1 = sp[r]
+            rng.append((a0, a1, r * n // P - a0, (r + 1) * n // P - a1))
+        res = []
+        for r in range(P):
+            a0, a1, b0, b1 = rng[r]
+            own = ov(a0, a1, r, sa) + ov(b0, b1, r, sb)
+            served = sum(ov(x[0], x[1], r, sa) + ov(x[2], x[3], r, sb)
+                         for q, x in enumerate(rng))
+            res.append({"in": (a1 - a0) + (b1 - b0) - own, "out": served - own,
+                        "hbm_read": served, "hbm_write": (a1 - a0) + (b1 - b0)})
+        return res
+
+    def __call__(self, out=None, out_vals=None):
         m = self.o1 - self.o0
         if out is None:
             out = torch.empty(m * (2 if self.kt == N.KEY_ELEMENT else 1),
@@ -424,17 +528,14 @@ class P2PMerger:
                               device=self.a.device)
         if out_vals is None and self.av is not None:
             out_vals = torch.empty(m, dtype=torch.uint32, device=self.a.device)
-        stream = torch.cuda.current_stream(self.a.device)
-        if sync:
-            stream.synchronize()
-            dist.barrier(group=self.comm.group)
+        st = torch.cuda.current_stream(self.a.device).cuda_stream
+        ranks = range(self.comm.world)
+        self.flags.arrive(_Flags.READY, ranks, st)
         N.check(N.lib.mp_merge_pieces(self.kt, self._arr_a, len(self.pa), self._arr_b,
                                       len(self.pb), self.o0, self.o1, out.data_ptr(),
                                       out_vals.data_ptr() if out_vals is not None else None,
-                                      stream.cuda_stream))
-        if sync:
-            stream.synchronize()
-            dist.barrier(group=self.comm.group)
+                                      st))
+        self.flags.arrive(_Flags.DONE, ranks, st)
         return out, out_vals
 
 
@@ -448,9 +549,11 @@ class P2PSorter:
     input order; an unpaired last block is carried, sort.hpp:98-100) and
     every rank of a pair merges its equal slice of the pair's output with
     mp_merge_pieces straight from the peers' mapped buffers into its pong
-    buffer.  A barrier closes each round (nobody overwrites a buffer a peer
-    may still read), then ping/pong swap.  Slice sizes are computed, not
-    communicated: every rank knows every length."""
+    buffer, then ping/pong swap.  Each round is ordered among the pair's
+    ranks on the GPU alone (_Flags READY before the merge, DONE after it:
+    nobody overwrites a buffer a peer may still read).  Slice sizes are
+    computed, not communicated: every rank knows every length (pass `lens`
+    to skip the one host all_gather of the shard sizes)."""
 
     def __init__(self, capacity: int, dtype, key_type: int, group=None, device=None):
         self.comm = _Comm(group)
@@ -463,14 +566,48 @@ class P2PSorter:
         recs = [None] * self.comm.world
         dist.all_gather_object(recs, (_export(self.buf[0]), _export(self.buf[1])), group=group)
         self.peer = [[0, 0] for _ in range(self.comm.world)]
+        self._imported = []
         for r, (e0, e1) in enumerate(recs):
             if r == self.comm.rank:
                 self.peer[r] = [self.buf[0].data_ptr(), self.buf[1].data_ptr()]
             else:
                 self.peer[r] = [_import(e0), _import(e1)]
+                self._imported += [x for x in self.peer[r] if x]
+        self.flags = _Flags(self.comm, dev)
+        self._imported += self.flags.imported
         self.scratch = None
 
-    def run(self, x_local: torch.Tensor, sync=True):
+    close = P2PMerger.close
+    __del__ = P2PMerger.__del__
+
+    @staticmethod
+    def schedule(lens):
+        """The rounds: for each round, (left ranks, right ranks, new lens) per
+        rank group, and each rank's output range in its group's merge."""
+        P = len(lens)
+        rounds, h = [], 1
+        while h < P:
+            new_lens = list(lens)
+            groups = []
+            for s in range(0, P, 2 * h):
+                L = list(range(s, min(s + h, P)))
+                R = list(range(s + h, min(s + 2 * h, P)))
+                if R:
+                    owners = L + R
+                    tot = sum(lens[q] for q in owners)
+                    for k, q in enumerate(owners):
+                        new_lens[q] = (k + 1) * tot // len(owners) - k * tot // len(owners)
+                groups.append((L, R, list(lens)))
+            rounds.append(groups)
+            lens = new_lens
+            h *= 2
+        return rounds, lens
+
+    def run(self, x_local: torch.Tensor, lens=None, trace=None):
+        """Sort; returns this rank's slice of the sorted sequence.  With a
+        list `trace`, each merge round appends (owners, k, o0, o1, splits)
+        -- the actual split points of this rank's slice, searched over the
+        round's mapped inputs (mp_pieces_partition) -- for sort_traffic()."""
         P, me = self.comm.world, self.comm.rank
         kt = self.kt
         n_me = n_keys(x_local, kt)
@@ -479,7 +616,10 @@ class P2PSorter:
             # an overrun would corrupt memory the peers read
             raise ValueError(f"P2PSorter.run: shard of {n_me} keys exceeds the capacity "
                              f"{self.capacity} set at construction")
-        lens = [x[0] for x in self.comm.all_gather_int([n_me])]
+        if lens is None:
+            lens = [x[0] for x in self.comm.all_gather_int([n_me])]
+        elif len(lens) != P or lens[me] != n_me:
+            raise ValueError("P2PSorter.run: lens must list every rank's shard size")
         stream = torch.cuda.current_stream(self.buf[0].device)
         st = stream.cuda_stream
         sb = N.lib.mp_sort_scratch_bytes(kt, 0, n_me)
@@ -487,47 +627,162 @@ class P2PSorter:
             self.scratch = torch.empty(max(sb, 16), dtype=torch.uint8, device=self.buf[0].device)
         N.check(N.lib.mp_sort_to(kt, x_local.data_ptr(), None, self.buf[0].data_ptr(), None,
                                  n_me, self.scratch.data_ptr(), self.scratch.numel(), st))
-        cur, h = 0, 1
-        while h < P:
-            if sync:
-                stream.synchronize()
-                dist.barrier(group=self.comm.group)
-            new_lens = list(lens)
-            s0 = (me // (2 * h)) * 2 * h
-            left = list(range(s0, min(s0 + h, P)))
-            right = list(range(s0 + h, min(s0 + 2 * h, P)))
-            for s in range(0, P, 2 * h):  # every block pair's new slice sizes
-                L = list(range(s, min(s + h, P)))
-                R = list(range(s + h, min(s + 2 * h, P)))
-                if R:
-                    owners = L + R
-                    tot = sum(lens[q] for q in owners)
-                    for k, q in enumerate(owners):
-                        new_lens[q] = (k + 1) * tot // len(owners) - k * tot // len(owners)
-            if right:
-                owners = left + right
+        rounds, final = self.schedule(lens)
+        cur = 0
+        for groups in rounds:
+            L, R, glens = next(g for g in groups if me in g[0] + g[1])
+            if R:
+                owners = L + R
                 k = owners.index(me)
-                tot = sum(lens[q] for q in owners)
+                tot = sum(glens[q] for q in owners)
                 o0, o1 = k * tot // len(owners), (k + 1) * tot // len(owners)
                 if o1 - o0 > self.capacity:  # an equal split never exceeds the largest shard
                     raise ValueError("P2PSorter.run: round slice exceeds the capacity")
-                pa = N.pieces_array([(self.peer[q][cur] if lens[q] else None, None, lens[q])
-                                     for q in left])
-                pb = N.pieces_array([(self.peer[q][cur] if lens[q] else None, None, lens[q])
-                                     for q in right])
-                N.check(N.lib.mp_merge_pieces(kt, pa, len(left), pb, len(right), o0, o1,
+                pa = N.pieces_array([(self.peer[q][cur] if glens[q] else None, None, glens[q])
+                                     for q in L])
+                pb = N.pieces_array([(self.peer[q][cur] if glens[q] else None, None, glens[q])
+                                     for q in R])
+                self.flags.arrive(_Flags.READY, owners, st)
+                if trace is not None:
+                    dev = self.buf[0].device
+                    d = torch.tensor([o0, o1], dtype=torch.int64, device=dev)
+                    sp = torch.empty(2, dtype=torch.int64, device=dev)
+                    N.check(N.lib.mp_pieces_partition(kt, pa, len(L), pb, len(R), d.data_ptr(),
+                                                      2, sp.data_ptr(), st))
+                    trace.append((owners, len(L), [glens[q] for q in owners], o0, o1, sp, d))
+                N.check(N.lib.mp_merge_pieces(kt, pa, len(L), pb, len(R), o0, o1,
                                               self.buf[1 - cur].data_ptr(), None, st))
+                self.flags.arrive(_Flags.DONE, owners, st)
             else:  # carried block: copy through so every rank sits in `1-cur`
-                words = lens[me] * (2 if kt == N.KEY_ELEMENT else 1)
+                words = glens[me] * (2 if kt == N.KEY_ELEMENT else 1)
                 self.buf[1 - cur][:words].copy_(self.buf[cur][:words])
-            lens = new_lens
+                self.flags.gen += 2  # keep the generation in step with the paired ranks
+                if trace is not None:
+                    trace.append(None)
             cur = 1 - cur
-            h *= 2
-        if sync:
-            stream.synchronize()
-            dist.barrier(group=self.comm.group)
-        words = lens[me] * (2 if kt == N.KEY_ELEMENT else 1)
+        words = final[me] * (2 if kt == N.KEY_ELEMENT else 1)
         return self.buf[cur][:words]
+
+
+def _overlap(lo, hi, s0, s1):
+    return max(0, min(hi, s1) - max(lo, s0))
+
+
+def sort_traffic(comm, trace, lens, run0=8192):
+    """Collective.  Per-rank, per-phase element counts of one P2PSorter.run
+    (from a traced run): phase 0 = the local sort (its algorithmic HBM
+    passes: block sort + ceil(log2(n/run0)) rounds, each reading and writing
+    every key once); phase k >= 1 = cross round k: NVLink-in (elements of my
+    slice on other ranks), NVLink-out (elements of my block read by others),
+    HBM (elements my HBM serves to me and my peers + my slice's writes).
+    Returns (phases, final lens) with phases[k][r] = dict(in, out, hbm)."""
+    P, me = comm.world, comm.rank
+    rows = [None if t is None else (t[3], t[4]) + tuple(t[5].tolist()) for t in trace]
+    groups = [None if t is None else (t[0], t[1], t[2]) for t in trace]
+    allrows = [None] * P
+    dist.all_gather_object(allrows, (rows, groups), group=comm.group)
+    rounds, _ = P2PSorter.schedule(lens)
+
+    def lens_at(k, r):  # rank r's block length entering round k
+        return rounds[k][0][2][r] if rounds[k] else lens[r]
+
+    phases = []
+    local = []
+    for r in range(P):
+        w, passes = run0, 1
+        while w < lens[r]:
+            w, passes = 2 * w, passes + 1
+        local.append({"in": 0, "out": 0, "hbm": 2 * lens[r] * passes})
+    phases.append(local)
+    for k in range(len(rounds)):
+        ph = [{"in": 0, "out": 0, "hbm": 0} for _ in range(P)]
+        # each rank's (a0, a1, b0, b1) in its group's A/B index spaces
+        rng = {}
+        for r in range(P):
+            rws, gps = allrows[r]
+            if rws[k] is None:  # carried block: a local copy
+                ph[r]["hbm"] += 2 * lens_at(k, r)
+                continue
+            o0, o1, a0, a1 = rws[k]
+            owners, nl, gl = gps[k]
+            rng[r] = (owners, nl, gl, a0, a1, o0 - a0, o1 - a1)
+        for r, (owners, nl, gl, a0, a1, b0, b1) in rng.items():
+            # piece extents of every owner in the group's A (left) / B (right) space
+            ext = {}
+            s = 0
+            for q, ln in zip(owners[:nl], gl[:nl]):
+                ext[q] = ("a", s, s + ln)
+                s += ln
+            s = 0
+            for q, ln in zip(owners[nl:], gl[nl:]):
+                ext[q] = ("b", s, s + ln)
+                s += ln
+            for q in owners:
+                side, s0, s1 = ext[q]
+                got = _overlap(a0, a1, s0, s1) if side == "a" else _overlap(b0, b1, s0, s1)
+                ph[q]["hbm"] += got          # q's HBM serves r's read
+                if q != r:
+                    ph[r]["in"] += got
+                    ph[q]["out"] += got
+            ph[r]["hbm"] += (a1 - a0) + (b1 - b0)  # r's slice written to its HBM
+        phases.append(ph)
+    return phases
+
+
+def roofline_time(phases, key_bytes, hbm_gbs, nvl_gbs):
+    """t_g = sum over phases of max(HBM_g / HBM peak,
+    NVin_g / NVLink, NVout_g / NVLink); returns (max_g t_g in s, [t_g])."""
+    P = len(phases[0])
+    tg = []
+    for g in range(P):
+        t = 0.0
+        for ph in phases:
+            x = ph[g]
+            t += max(x["hbm"] * key_bytes / (hbm_gbs * 1e9),
+                     x["in"] * key_bytes / (nvl_gbs * 1e9),
+                     x["out"] * key_bytes / (nvl_gbs * 1e9))
+        tg.append(t)
+    return max(tg), tg
+
+
+def nvlink_probe(comm, device, mib=1024, reps=5):
+    """Measured NVLink pull rate: every rank reads `mib` MiB from rank
+    (r+1) % P's HBM into its own with SM vector loads (mp_peer_copy, the
+    peer loader's access pattern), all ranks at once; CUDA events on the
+    launching stream.  Returns (GB/s per rank, min over ranks).  On one GPU
+    shared by several ranks it measures same-device IPC copies."""
+    P, me = comm.world, comm.rank
+    nbytes = mib << 20
+    src = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    src.fill_(me & 0xFF)
+    recs = [None] * P
+    dist.all_gather_object(recs, _export(src), group=comm.group)
+    peer = _import(recs[(me + 1) % P]) if P > 1 else src.data_ptr()
+    flags = _Flags(comm, device)
+    st = torch.cuda.current_stream(device)
+    ranks = range(P)
+    rates = []
+    for i in range(reps + 1):
+        flags.arrive(_Flags.READY, ranks, st.cuda_stream)  # all ranks start together
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        N.check(N.lib.mp_peer_copy(dst.data_ptr(), peer, nbytes, st.cuda_stream))
+        e1.record(st)
+        flags.arrive(_Flags.DONE, ranks, st.cuda_stream)
+        st.synchronize()
+        if i:  # first pull warms the mapping
+            rates.append(nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    if P > 1:
+        N.check(N.lib.mp_ipc_close(peer))
+    for x in flags.imported:
+        N.check(N.lib.mp_ipc_close(x))
+    import statistics
+    mine = statistics.median(rates)
+    allr = comm.all_gather_int([int(mine * 1000)])
+    per_rank = [x[0] / 1000 for x in allr]
+    return per_rank, min(per_rank)
 
 
 # --------------------------------------------------------------------------
@@ -600,7 +855,7 @@ def sharded_sort(x_local: torch.Tensor, vals=None, key_type=None, group=None,
 
 
 # --------------------------------------------------------------------------
-# bench.py --gpus N (N > 1): weak scaling, one process per GPU over NCCL
+# bench.py --gpus N (N > 1): one process per GPU over NCCL
 # --------------------------------------------------------------------------
 class _NoClock:
     def __enter__(self):
@@ -613,19 +868,69 @@ class _NoClock:
         return None
 
 
-def bench_distributed(args, cfg, ws, rank, local, clock=None):
-    """Each rank holds a fixed-size shard (the config's |A| and |B| per GPU)
-    of globally sorted A and B (generated with the SplitMix64 counter
-    generator at the rank's global offsets, then sorted across the ranks
-    with sharded_sort -- untimed).  A timed step is one sharded_merge: joint
-    split search + NVLink exchange + local K1/K2 merge.  Max over ranks."""
+def _peaks():
     import json
-    import statistics
-    import time
     from pathlib import Path
+    f = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+    if f.exists():
+        return float(json.loads(f.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
+
+def _time_steps(step, steps, warmup, comm, red_dev, clock):
+    """W untimed steps, then EXACTLY `steps` steps between a barrier +
+    synchronize on both sides, timed with CUDA events on the launching
+    stream; returns the max over ranks in ms and the launches counted."""
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier(group=comm.group)
+    st = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    c0 = N.lib.mp_launch_count()
+    with (clock or _NoClock)() as clk:
+        e0.record(st)
+        for _ in range(steps):
+            step()
+        e1.record(st)
+        torch.cuda.synchronize()
+    launches = N.lib.mp_launch_count() - c0
+    dist.barrier(group=comm.group)
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=red_dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=comm.group)
+    return float(ms.item()), launches, clk.summary()
+
+
+def _nvl(comm, dev, shrink):
+    """The NVLink rate the roofline is computed against: measured here
+    (nvlink_probe) -- ranks sharing one GPU (MP_BENCH_DEVICE) measure a
+    same-device copy, which is said in the source field."""
+    import os
+    try:
+        per, low = nvlink_probe(comm, dev, mib=max(16, 1024 >> shrink))
+        shared = "MP_BENCH_DEVICE" in os.environ
+        src = ("measured in this run: mp_peer_copy pull from rank (r+1)%P, all ranks at once"
+               + (" (ranks share ONE GPU: same-device copy, not NVLink)" if shared else ""))
+        return low, per, src
+    except Exception as e:  # pragma: no cover
+        return 900.0, None, f"spec 900 GB/s per direction (probe failed: {e})"
+
+
+def bench_distributed(args, cfg, ws, rank, local, clock=None):
+    """A merge config at N GPUs.  Configs 2/3 (weak scaling): each rank
+    holds the config's |A| and |B| as its shard of globally sorted A and B
+    (SplitMix64 counter generator at the rank's global offsets, then sorted
+    across the ranks with sharded_sort -- untimed).  Config 5 (strong
+    scaling): the fixed 2^31 + 2^31 f32 inputs sharded contiguously.  A
+    timed step is one P2PMerger call: each rank merges its output slice
+    straight from the mapped shards (NVLink pull fused into the tile loads),
+    ordered across ranks by stream flags only.  Max over ranks."""
+    import os
+    import time
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    comm = _Comm()
     kt = {"u32": N.KEY_U32, "i32": N.KEY_I32, "f32": N.KEY_F32, "u64": N.KEY_U64,
           "i64": N.KEY_I64}[cfg["key"]]
     dt = {"u32": torch.uint32, "i32": torch.int32, "f32": torch.float32,
@@ -637,12 +942,9 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
         N.check(N.lib.mp_generate(kind, seed, first, n, x.data_ptr(), st))
         return x
 
-    import os
-    # MP_BENCH_SCALE=k shrinks the per-GPU sizes by 2^k (multi-rank smoke
-    # tests on a one-GPU box); reductions go through the backend's device
+    # MP_BENCH_SCALE=k shrinks the sizes by 2^k (multi-rank smoke tests on
+    # a one-GPU box)
     shrink = int(os.environ.get("MP_BENCH_SCALE", "0"))
-    # config 5 fixes the global sizes (sharded over the ranks: strong
-    # scaling); the others fix the per-GPU sizes (weak scaling)
     strong = bool(cfg.get("sharded"))
     NA, NB = cfg["na"] >> shrink, cfg["nb"] >> shrink
     if strong:
@@ -659,69 +961,51 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
     if cfg.get("vals"):
         # config 3 payload: each key's index in its globally sorted array
         # (bit 31 set on B's), as in the single-GPU bench
-        comm = _Comm()
         la = [x[0] for x in comm.all_gather_int([a.numel()])]
         lb = [x[0] for x in comm.all_gather_int([b.numel()])]
         av = (torch.arange(a.numel(), dtype=torch.int64, device=dev) + sum(la[:rank])
               ).to(torch.int32).view(torch.uint32)
         bv = ((torch.arange(b.numel(), dtype=torch.int64, device=dev) + sum(lb[:rank]))
               | (1 << 31)).to(torch.int32).view(torch.uint32)
-    transport = getattr(args, "transport", "p2p")
-    if transport == "p2p":
-        merger = P2PMerger(a, b, av, bv, key_type=kt)  # IPC mappings built once (untimed)
-        step = lambda: merger()  # noqa: E731
-    else:
-        step = lambda: sharded_merge(a, b, av, bv, key_type=kt)  # noqa: E731
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    times = []
-    c0 = N.lib.mp_launch_count()
-    with (clock or _NoClock)() as clk:
-        for _ in range(args.steps):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            out, _ = step()
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-    launches = N.lib.mp_launch_count() - c0
-    dist.barrier()
-    ms = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    merger = P2PMerger(a, b, av, bv, key_type=kt)  # IPC mappings + flags, once (untimed)
+    out = torch.empty(merger.o1 - merger.o0, dtype=dt, device=dev)
+    outv = torch.empty(out.numel(), dtype=torch.uint32, device=dev) if av is not None else None
+    step = lambda: merger(out, outv)  # noqa: E731
+    ms, launches, clk = _time_steps(step, args.steps, args.warmup, comm, red_dev, clock)
     total = (NA + NB) if strong else (na + nb) * ws
     value = total * args.steps / (ms / 1e3)
-    # e2e through the public API with host buffers: H2D shard, sharded merge,
-    # D2H of this rank's output slice (wall clock, max over ranks)
+    # traffic from the actual split points, HBM + NVLink roofline
+    tr = merger.traffic()
+    hbm, hbm_src = _peaks()
+    nvl, nvl_per, nvl_src = _nvl(comm, dev, shrink)
+    ks = a.element_size() + (4 if av is not None else 0)  # key (+ value) bytes
+    t_roof, tg = roofline_time([tr], ks, hbm, nvl)
+    # e2e through the public API with host buffers: H2D of this rank's
+    # shards, the sharded merge, D2H of its output slice (wall clock, max
+    # over ranks)
     ha, hb = a.cpu().pin_memory(), b.cpu().pin_memory()
     hav = av.cpu().pin_memory() if av is not None else None
     hbv = bv.cpu().pin_memory() if bv is not None else None
+    ho = torch.empty(out.numel(), dtype=dt).pin_memory()
+    hov = torch.empty(out.numel(), dtype=torch.uint32).pin_memory() if av is not None else None
     e2e_steps = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
+    torch.cuda.synchronize()
     dist.barrier()
     t = time.perf_counter()
     for _ in range(e2e_steps):
-        a.copy_(ha, non_blocking=True)  # H2D into the registered shards
+        a.copy_(ha, non_blocking=True)  # H2D into the mapped shards
         b.copy_(hb, non_blocking=True)
         if hav is not None:
             av.copy_(hav, non_blocking=True)
             bv.copy_(hbv, non_blocking=True)
-        o, ov = step()
-        ho = o.cpu()
-        if ov is not None:
-            ho = ov.cpu()
+        merger(out, outv)
+        ho.copy_(out, non_blocking=True)
+        if hov is not None:
+            hov.copy_(outv, non_blocking=True)
     torch.cuda.synchronize()
     el = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=red_dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    ks = a.element_size() + (4 if av is not None else 0)  # key (+ value) bytes
-    peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json")
-                      .read_text())["hbm_gbs"] if (Path(__file__).resolve().parents[1] /
-                                                   "MEASURED_PEAKS.json").exists() else 6650.0
-    per_rank_bytes = (na + nb) * 2 * ks
-    achieved = per_rank_bytes / (ms / args.steps / 1e3) / 1e9
-    del ho, statistics
+    merger.close()
     return {
         "metric": "merged elements/s", "value": value, "unit": "elements/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -731,18 +1015,25 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
         "data": "synthetic: SplitMix64 counter generator, globally sorted with sharded_sort",
         "config": {"workload": cfg["desc"] + (f"; sharded over {ws} GPUs" if strong else
                                              f" per GPU; global |A|={NA * ws} |B|={NB * ws}"),
-                   "parallelism": f"merge-path diagonal split over {ws} GPUs ("
-                                  + ("NVLink pull fused into the merge kernels via CUDA IPC"
-                                     if transport == "p2p" else "NCCL all_to_all exchange") + ")",
+                   "parallelism": f"merge-path diagonal split over {ws} GPUs (NVLink pull "
+                                  "fused into the merge kernels via CUDA IPC; stream-flag "
+                                  "ordering, no host sync per step)",
                    "l2": "inputs+output larger than L2 (no flush needed)"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm+nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "note": "per-rank algorithmic HBM bytes / step time; the exchange also "
-                             "moves up to 4 B per remote element over NVLink"},
-        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm+nvlink", "unit": "elements/s", "achieved": value,
+                     "peak": total / t_roof, "frac": value / (total / t_roof),
+                     "traffic": None,
+                     "model": "N / max_g max(HBM_g/hbm_gbs, NVin_g/nvlink_gbs, NVout_g/nvlink_gbs)"
+                              " from the actual split points",
+                     "hbm_gbs": hbm, "hbm_source": hbm_src, "nvlink_gbs": nvl,
+                     "nvlink_source": nvl_src, "nvlink_gbs_per_rank": nvl_per,
+                     "t_g_ms": [x * 1e3 for x in tg]},
+        "nvlink": {"in_bytes_per_rank": [x["in"] * ks for x in tr],
+                   "out_bytes_per_rank": [x["out"] * ks for x in tr],
+                   "hbm_bytes_per_rank": [(x["hbm_read"] + x["hbm_write"]) * ks for x in tr]},
+        "clocks": clk,
         "e2e": {"value": total * e2e_steps / float(el.item()), "unit": "elements/s",
-                "h2d_bytes_per_step": (na + nb) * ks, "d2h_bytes_per_step": (na + nb) * ks},
+                "h2d_bytes_per_step": (na + nb) * ks, "d2h_bytes_per_step": out.numel() * ks},
     }
 
 
@@ -756,67 +1047,67 @@ def bench_distributed_sort(args, cfg, ws, rank, local, clock=None):
     import time
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    comm = _Comm()
     shrink = int(os.environ.get("MP_BENCH_SCALE", "0"))
     n = cfg["n"] >> shrink
     lo, hi = rank * n // ws, (rank + 1) * n // ws
+    lens = [(r + 1) * n // ws - r * n // ws for r in range(ws)]
     x = torch.empty(hi - lo, dtype=torch.uint32, device=dev)
     st = torch.cuda.current_stream().cuda_stream
     N.check(N.lib.mp_generate(cfg["gen"][0], 4, lo, hi - lo, x.data_ptr(), st))
-    sorter = P2PSorter((n + ws - 1) // ws + 1, torch.uint32, N.KEY_U32)
-    for _ in range(args.warmup):
-        sorter.run(x)
-    torch.cuda.synchronize()
-    dist.barrier()
-    times = []
-    c0 = N.lib.mp_launch_count()
-    with (clock or _NoClock)() as clk:
-        for _ in range(args.steps):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            sorter.run(x)
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-    launches = N.lib.mp_launch_count() - c0
+    sorter = P2PSorter(max(lens) + 1, torch.uint32, N.KEY_U32)
     red_dev = dev if dist.get_backend() == "nccl" else torch.device("cpu")
-    ms = torch.tensor([sum(times)], dtype=torch.float64, device=red_dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    ms, launches, clk = _time_steps(lambda: sorter.run(x, lens), args.steps, args.warmup,
+                                    comm, red_dev, clock)
+    # traced run (untimed): the actual split points of every round
+    trace = []
+    sorter.run(x, lens, trace=trace)
+    torch.cuda.synchronize()
+    phases = sort_traffic(comm, trace, lens)
+    hbm, hbm_src = _peaks()
+    nvl, nvl_per, nvl_src = _nvl(comm, dev, shrink)
+    t_roof, tg = roofline_time(phases, 4, hbm, nvl)
     # e2e: pinned host shard -> device, sort, sorted slice back to the host
     hx = x.cpu().pin_memory()
+    _, final = P2PSorter.schedule(lens)
+    ho = torch.empty(final[rank], dtype=torch.uint32).pin_memory()
+    e2e_steps = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
+    torch.cuda.synchronize()
     dist.barrier()
     t = time.perf_counter()
-    e2e_steps = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
     for _ in range(e2e_steps):
         x.copy_(hx, non_blocking=True)
-        o = sorter.run(x)
-        ho = o.cpu()
+        ho.copy_(sorter.run(x, lens), non_blocking=True)
     torch.cuda.synchronize()
     el = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=red_dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
-    del ho
-    rounds, w = 0, 8192  # mp_sort's bare 32-bit block-sort run
-    while w < (n + ws - 1) // ws:
-        w, rounds = 2 * w, rounds + 1
-    passes = 1 + rounds + (ws - 1).bit_length()
+    sorter.close()
+    value = n * args.steps / (ms / 1e3)
     return {
-        "metric": "merge-sort keys/s", "value": n * args.steps / (ms / 1e3), "unit": "keys/s",
+        "metric": "merge-sort keys/s", "value": value, "unit": "keys/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32",
         "data": "synthetic: SplitMix64 counter generator, seed 4",
         "config": {"workload": cfg["desc"] + f"; {ws} GPUs, 1/{ws} shard each",
                    "parallelism": f"local sort + {(ws - 1).bit_length()} cross-GPU Merge Path "
-                                  "rounds, NVLink pull fused into the merge (CUDA IPC)",
+                                  "rounds, NVLink pull fused into the merge (CUDA IPC), "
+                                  "stream-flag ordering",
                    "l2": "inputs+output larger than L2 (no flush needed)"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm+nvlink", "unit": "GB/s",
-                     "achieved": (n // ws) * 8 * passes / (ms / args.steps / 1e3) / 1e9,
-                     "peak": 6554.2, "frac": (n // ws) * 8 * passes / (ms / args.steps / 1e3)
-                     / 1e9 / 6554.2, "traffic": None,
-                     "note": f"per-GPU {passes} passes x 8 B/key over the step time"},
-        "clocks": clk.summary(),
+        "roofline": {"bound": "hbm+nvlink", "unit": "keys/s", "achieved": value,
+                     "peak": n / t_roof, "frac": value / (n / t_roof), "traffic": None,
+                     "model": "N / max_g sum_phases max(HBM_g/hbm_gbs, NVin_g/nvlink_gbs, "
+                              "NVout_g/nvlink_gbs); local sort = (1 + rounds) passes x 8 B/key, "
+                              "cross rounds from the traced split points",
+                     "hbm_gbs": hbm, "hbm_source": hbm_src, "nvlink_gbs": nvl,
+                     "nvlink_source": nvl_src, "nvlink_gbs_per_rank": nvl_per,
+                     "t_g_ms": [t * 1e3 for t in tg]},
+        "nvlink": {"in_bytes_per_rank": [sum(ph[r]["in"] for ph in phases) * 4
+                                         for r in range(ws)],
+                   "out_bytes_per_rank": [sum(ph[r]["out"] for ph in phases) * 4
+                                          for r in range(ws)]},
+        "clocks": clk,
         "e2e": {"value": n * e2e_steps / float(el.item()), "unit": "keys/s",
-                "h2d_bytes_per_step": (hi - lo) * 4, "d2h_bytes_per_step": (hi - lo) * 4},
+                "h2d_bytes_per_step": (hi - lo) * 4, "d2h_bytes_per_step": final[rank] * 4},
     }

@@ -37,8 +37,10 @@ def test_merge_pieces_in_process(cuda, port, kt_name):
     rng = np.random.default_rng(41)
     kt = key_type(kt_name)
     st = torch.cuda.current_stream().cuda_stream
+    # the last two: every tile straddles several (often empty) pieces
     for na, nb, npa, npb, dup in ((50_000, 37_001, 3, 5, 100), (200_001, 0, 4, 1, 7),
-                                  (1 << 20, 1 << 19, 8, 8, 1 << 30), (5, 300_000, 2, 16, 3)):
+                                  (1 << 20, 1 << 19, 8, 8, 1 << 30), (5, 300_000, 2, 16, 3),
+                                  (40, 33, 16, 16, 5), (3000, 2999, 16, 11, 1 << 20)):
         a = _rand_sorted(kt_name, rng, na, dup)
         b = _rand_sorted(kt_name, rng, nb, dup)
         if kt_name == "el":
@@ -90,15 +92,16 @@ def test_merge_pieces_with_values(cuda, port):
             s += ln
         return N.pieces_array(out)
 
-    sa, sb = [100_000, 0, 200_000], [1, 50_000, 50_002]
-    pa, pb = pieces(a, av, sa), pieces(b, bv, sb)
-    out = torch.empty(na + nb, dtype=torch.uint64, device=cuda)
-    outv = torch.empty(na + nb, dtype=torch.uint32, device=cuda)
-    N.check(N.lib.mp_merge_pieces(N.KEY_U64, pa, 3, pb, 3, 0, na + nb, out.data_ptr(),
-                                  outv.data_ptr(), st))
-    torch.cuda.synchronize()
-    assert np.array_equal(out.cpu().numpy(), want)
-    assert np.array_equal(outv.cpu().numpy(), wantv)
+    for sa, sb in (([100_000, 0, 200_000], [1, 50_000, 50_002]),
+                   ([1, 2, 3, 0, 5, 299_989], [7, 0, 0, 100_003 - 11, 1, 3])):
+        pa, pb = pieces(a, av, sa), pieces(b, bv, sb)
+        out = torch.empty(na + nb, dtype=torch.uint64, device=cuda)
+        outv = torch.empty(na + nb, dtype=torch.uint32, device=cuda)
+        N.check(N.lib.mp_merge_pieces(N.KEY_U64, pa, len(sa), pb, len(sb), 0, na + nb,
+                                      out.data_ptr(), outv.data_ptr(), st))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), want)
+        assert np.array_equal(outv.cpu().numpy(), wantv)
 
 
 def _free_port() -> int:
@@ -241,8 +244,9 @@ def test_distributed_bench_two_ranks(cuda, config):
     """bench.py --gpus 2 through torchrun (both ranks on the box's one GPU,
     gloo plumbing, inputs shrunk 2^5): the fused P2P merge (config 2, weak
     scaling; config 5, f32, the fixed global size sharded) and the P2P sort
-    (config 4) run and print one JSON line with the library's launch count;
-    config 3a carries its u32 values through the fused merge."""
+    (config 4) run and print one JSON line with the library's launch count,
+    the per-rank NVLink bytes from the actual split points and the
+    HBM + NVLink roofline; config 2 also carries config 5 and the sort."""
     import json
     import subprocess
     env = dict(os.environ, MP_BENCH_DEVICE="0", MP_BENCH_BACKEND="gloo", MP_BENCH_SCALE="5")
@@ -250,10 +254,36 @@ def test_distributed_bench_two_ranks(cuda, config):
                         "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
                         str(_free_port()), "bench.py", "--config", config, "--gpus", "2",
                         "--steps", "2", "--warmup", "1"], capture_output=True, text=True,
-                       timeout=600, env=env, cwd=str(ROOT))
+                       timeout=900, env=env, cwd=str(ROOT))
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
     assert d["scaling"] == ("weak" if config in ("2", "3a") else "strong")
+    recs = [d] + ([d["config5"], d["sort"]] if config == "2" else [])
+    for x in recs:
+        rf = x["roofline"]
+        assert rf["bound"] == "hbm+nvlink" and rf["nvlink_gbs"] > 0 and rf["peak"] > 0
+        assert 0 < rf["frac"] and len(rf["t_g_ms"]) == 2
+        assert len(x["nvlink"]["in_bytes_per_rank"]) == 2
+    if config == "5":  # the ranks' output slices need the other rank's shards
+        assert sum(d["nvlink"]["in_bytes_per_rank"]) > 0
+
+
+def test_bench_gpus_flag_spawns_ranks(cuda):
+    """`python bench.py --gpus 2` with no launcher starts its own two ranks
+    (never silently runs one GPU); a WORLD_SIZE that disagrees is an error."""
+    import json
+    import subprocess
+    env = dict(os.environ, MP_BENCH_DEVICE="0", MP_BENCH_BACKEND="gloo", MP_BENCH_SCALE="6")
+    r = subprocess.run([sys.executable, "bench.py", "--config", "4", "--gpus", "2", "--steps",
+                        "2", "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                       env=env, cwd=str(ROOT))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
+    bad = subprocess.run([sys.executable, "bench.py", "--gpus", "4"], capture_output=True,
+                         text=True, timeout=120, cwd=str(ROOT),
+                         env=dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0"))
+    assert bad.returncode == 2
