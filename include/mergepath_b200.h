@@ -187,6 +187,39 @@ int mp_merge_pieces(int key_type, const mp_piece *a, int na_pieces,
                     uint64_t out_end, void *out, uint32_t *out_vals,
                     void *stream);
 
+/* ---- multi-GPU in one process: shard tables --------------------------- */
+/* A shard of a sequence on one GPU (keys, optional values: device pointers
+ * on `device`). */
+typedef struct mp_shard {
+  int device;
+  void *keys;
+  uint32_t *vals;
+  uint64_t len;
+} mp_shard;
+
+/* Stable merge of A = a[0] ++ ... ++ a[na-1] and B = b[0] ++ ... (each 1..16
+ * shards, any devices) into the output shards: out[g] receives merged
+ * positions [len(out[0..g)), + out[g].len) and is computed ON out[g].device,
+ * its windows read straight from the input shards' devices (peer access is
+ * enabled; NVLink pull inside the tile loads).  sum(out.len) must equal
+ * |A| + |B| (parallel.hpp:155-156).  Values ride along when out[0].vals is
+ * non-NULL (then every non-empty shard carries them).
+ * streams == NULL: blocking (all involved devices synchronised at entry,
+ * the call returns when the output is complete).  Otherwise streams[g] (on
+ * out[g].device) for each output shard: asynchronous, ordered after all
+ * prior work on every given stream and before all later work on any of
+ * them (cross-device events), so inputs may be produced on those streams. */
+int mp_multi_merge(int key_type, const mp_shard *a, int na, const mp_shard *b, int nb,
+                   const mp_shard *out, int nout, void *const *streams);
+/* In-place stable sort of X = x[0] ++ ... ++ x[P-1] (P = 1..16 shards, any
+ * devices; values ride along when x[0].vals is non-NULL): afterwards x[g]
+ * holds sorted positions [len(x[0..g)), + x[g].len).  Each shard is sorted
+ * on its device (mp_sort), then ceil(log2 P) rounds merge rank groups
+ * (left group = A: stable w.r.t. the input order) with every shard keeping
+ * its length; one scratch buffer per shard from the library pool.
+ * `streams` as for mp_multi_merge (one per shard). */
+int mp_multi_sort(int key_type, const mp_shard *x, int P, void *const *streams);
+
 /* a_offs[k] = a_off of the merge path of the piece lists on diagonal
  * diags[k] (clamped to |A| + |B|): the multi-GPU analogue of
  * mp_diagonal_search (diags and a_offs are device arrays).  Used to place a

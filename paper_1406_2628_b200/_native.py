@@ -57,6 +57,8 @@ SIGNATURES = [
     ("mp_merge_checksum_host", _i, [_i, _p, _u64, _p, _u64, _p, _i]),
     ("mp_merge_pieces", _i, [_i, _p, _i, _p, _i, _u64, _u64, _p, _p, _p]),
     ("mp_pieces_partition", _i, [_i, _p, _i, _p, _i, _p, _u64, _p, _p]),
+    ("mp_multi_merge", _i, [_i, _p, _i, _p, _i, _p, _i, _p]),
+    ("mp_multi_sort", _i, [_i, _p, _i, _p]),
     ("mp_peer_copy", _i, [_p, _p, _u64, _p]),
     ("mp_ipc_export", _i, [_p, _p, _p]),
     ("mp_ipc_import", _i, [_p, _u64, _p]),
@@ -117,4 +119,18 @@ def pieces_array(pieces):
     arr = (Piece * max(1, len(pieces)))()
     for k, (kp, vp, n) in enumerate(pieces):
         arr[k].keys, arr[k].vals, arr[k].len = kp, vp, n
+    return arr
+
+
+class Shard(C.Structure):
+    """mp_shard: a shard of a sequence on one GPU."""
+    _fields_ = [("device", C.c_int), ("keys", C.c_void_p), ("vals", C.c_void_p),
+                ("len", C.c_uint64)]
+
+
+def shards_array(shards):
+    """[(device, keys_ptr, vals_ptr_or_None, len)] -> ctypes mp_shard array."""
+    arr = (Shard * max(1, len(shards)))()
+    for k, (d, kp, vp, n) in enumerate(shards):
+        arr[k].device, arr[k].keys, arr[k].vals, arr[k].len = d, kp, vp, n
     return arr

@@ -118,6 +118,19 @@ int alloc_scratch(ScratchGuard &g, size_t bytes, cudaStream_t s) {
   return MP_OK;
 }
 
+struct DeviceScope {  // restores the caller's current device
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceScope(int dev) {
+    cudaGetDevice(&prev);
+    err = cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    if (prev >= 0)
+      cudaSetDevice(prev);
+  }
+};
+
 uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 template <class KT> bool aligned_keys(const void *p) {
@@ -1278,6 +1291,10 @@ template <class KT> struct PiecesOp {
   }
 };
 
+}  // namespace
+#include "mp_multi.cuh"
+namespace {
+
 template <class KT> struct PiecesDiagOp {
   static int run(const mp_piece *pa, int npa, const mp_piece *pb, int npb,
                  const uint64_t *diags, uint64_t count, uint64_t *a_offs, cudaStream_t s) {
@@ -1336,18 +1353,6 @@ cudaStream_t host_stream(int device) {
   return streams[device];
 }
 
-struct DeviceScope {  // restores the caller's current device
-  int prev = -1;
-  cudaError_t err = cudaSuccess;
-  explicit DeviceScope(int dev) {
-    cudaGetDevice(&prev);
-    err = cudaSetDevice(dev);
-  }
-  ~DeviceScope() {
-    if (prev >= 0)
-      cudaSetDevice(prev);
-  }
-};
 
 // ---------------------------------------------------------------------------
 // Host-buffer merge, pipelined over PCIe.
@@ -1688,6 +1693,21 @@ int mp_merge_pieces(int kt, const mp_piece *a, int na_pieces,
     return fail(MP_ERR_INVALID, "merge_pieces: NULL array");
   return dispatch<PiecesOp>(kt, a, na_pieces, b, nb_pieces, out_begin, out_end,
                             out, out_vals, static_cast<cudaStream_t>(stream));
+}
+
+int mp_multi_merge(int kt, const mp_shard *a, int na, const mp_shard *b, int nb,
+                   const mp_shard *out, int nout, void *const *streams) {
+  g_err.clear();
+  if (!a || !b || !out)
+    return fail(MP_ERR_INVALID, "multi_merge: NULL shard table");
+  return dispatch<MultiMergeOp>(kt, a, na, b, nb, out, nout, streams);
+}
+
+int mp_multi_sort(int kt, const mp_shard *shards, int P, void *const *streams) {
+  g_err.clear();
+  if (!shards)
+    return fail(MP_ERR_INVALID, "multi_sort: NULL shard table");
+  return dispatch<MultiSortOp>(kt, shards, P, streams);
 }
 
 int mp_pieces_partition(int kt, const mp_piece *a, int na_pieces, const mp_piece *b,

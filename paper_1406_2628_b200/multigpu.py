@@ -517,7 +517,8 @@ class P2PMerger:
             served = sum(ov(x[0], x[1], r, sa) + ov(x[2], x[3], r, sb)
                          for q, x in enumerate(rng))
             res.append({"in": (a1 - a0) + (b1 - b0) - own, "out": served - own,
-                        "hbm_read": served, "hbm_write": (a1 - a0) + (b1 - b0)})
+                        "hbm_read": served, "hbm_write": (a1 - a0) + (b1 - b0),
+                        "hbm": served + (a1 - a0) + (b1 - b0)})
         return res
 
     def __call__(self, out=None, out_vals=None):
@@ -1030,7 +1031,7 @@ def bench_distributed(args, cfg, ws, rank, local, clock=None):
                      "t_g_ms": [x * 1e3 for x in tg]},
         "nvlink": {"in_bytes_per_rank": [x["in"] * ks for x in tr],
                    "out_bytes_per_rank": [x["out"] * ks for x in tr],
-                   "hbm_bytes_per_rank": [(x["hbm_read"] + x["hbm_write"]) * ks for x in tr]},
+                   "hbm_bytes_per_rank": [x["hbm"] * ks for x in tr]},
         "clocks": clk,
         "e2e": {"value": total * e2e_steps / float(el.item()), "unit": "elements/s",
                 "h2d_bytes_per_step": (na + nb) * ks, "d2h_bytes_per_step": out.numel() * ks},
