@@ -69,6 +69,26 @@ def build_tool(verbose: bool = False) -> Path:
     return TOOL
 
 
+MULTI_SRC = ROOT / "tests" / "cpp" / "test_multi_gpu.cpp"
+MULTI_TEST = PKG / "bin" / "test_multi_gpu"
+
+
+def build_multi_test(verbose: bool = False) -> Path:
+    """The C++ caller of mp_multi_merge / mp_multi_sort (no Python)."""
+    MULTI_TEST.parent.mkdir(exist_ok=True)
+    cxx = shutil.which("g++") or "g++"
+    cmd = [cxx, "-std=c++17", "-O2", "-Wall", "-Wextra",
+           "-I", str(ROOT / "include"), "-I", str(CUDA_HOME / "include"),
+           "-o", str(MULTI_TEST) + ".tmp", str(MULTI_SRC),
+           "-L", str(PKG), "-lmergepath_b200", "-Wl,-rpath,$ORIGIN/..",
+           "-L", str(CUDA_HOME / "lib64"), "-lcudart_static", "-ldl", "-lrt", "-pthread"]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True, cwd=ROOT)
+    os.replace(str(MULTI_TEST) + ".tmp", MULTI_TEST)
+    return MULTI_TEST
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if force or not up_to_date():
         cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(LIB) + ".tmp", str(CSRC / "mp_capi.cu")]
@@ -80,6 +100,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             LIB.stat().st_mtime, TOOL_SRC.stat().st_mtime,
             *(p.stat().st_mtime for p in (ROOT / "include").rglob("*.h*"))):
         build_tool(verbose)
+    if force or not MULTI_TEST.exists() or MULTI_TEST.stat().st_mtime < max(
+            LIB.stat().st_mtime, MULTI_SRC.stat().st_mtime):
+        build_multi_test(verbose)
     return LIB
 
 
