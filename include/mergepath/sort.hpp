@@ -2,16 +2,19 @@
 
 // Drop-in replacement for the reference's mergepath/sort.hpp
 // (/root/reference/proj/include/mergepath/sort.hpp) backed by the B200
-// library.  Both sorts are one call to mp_sort_host: a stable 2048-key
-// register/shared-memory block sort (K3) followed by Merge Path rounds
-// (K4 round split points + K2 tile merge), left run = A in every pair so the
-// result is stable with respect to input index -- the same bytes as the
-// reference's plain and cache-efficient sorts (test_sort.cpp:128-135).
+// library.  Both sorts are one call to mp_sort_host, which runs mp_sort's
+// schedule on the device: a block sort into sorted runs -- K3w (8192-key
+// runs, bare 32-bit keys: u32 / i32 / f32) or the stable K3 (2048-key runs:
+// values, 64-bit keys, element) -- then ceil(log2(N / run)) Merge Path
+// rounds, run as fused round pairs (one HBM pass per two rounds, mp_quad.cuh)
+// for large bare 32-bit sorts and as K4 split points + K2 tile merges
+// otherwise; left run = A in every pair, so the result is stable with
+// respect to input index -- the same bytes as the reference's plain and
+// cache-efficient sorts (test_sort.cpp:128-135).
 //
 // make_sort_plan() still describes the REFERENCE CPU plan (32-element base
 // runs or C/3 blocks) so sort_stats::merge_rounds keeps its meaning for
-// drop-in callers (test_sort.cpp:27-67 pins it); the GPU schedule is
-// ceil(log2(N / 2048)) rounds.
+// drop-in callers (test_sort.cpp:27-67 pins it).
 
 #include <bit>
 #include <cstdint>

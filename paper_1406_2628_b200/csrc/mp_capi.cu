@@ -21,7 +21,6 @@
 #include <vector>
 
 #include "mp_kernels.cuh"
-#include "mp_spm.cuh"
 #include "mp_pieces.cuh"
 #include "mp_bsort.cuh"
 #include "mp_quad.cuh"
@@ -189,10 +188,6 @@ template <class KT> struct SortMergeCfg {
 constexpr int kBlockNT = 128;
 constexpr int kBlockVT = 16;
 constexpr uint64_t kRun = kBlockNT * kBlockVT;  // 2048-key block-sort runs
-// bare 32-bit keys: K3b (mp_bsort.cuh), 4096-key runs
-constexpr int kBareNT = 256;
-constexpr int kBareVT = 17;  // odd: conflict-free strided smem stores
-constexpr uint64_t kBareRun = kBareNT * kBareVT;
 // bare 32-bit keys: K3w (mp_bsort.cuh), 16 keys per thread
 #ifndef MP_WARP_NT
 #define MP_WARP_NT 512  // 8192-key runs: one round fewer (17 at 2^30) for
@@ -216,19 +211,6 @@ constexpr int kBigTileNT = 384;       // 384 x 23 >= 8192
 #endif
 constexpr int kQuadNT = MP_QUAD_NT;
 constexpr int kQuadVT = MP_QUAD_VT;
-// K5e2 (two merge slots per thread): 2 * kQuad2NT * kQuadVT >= 8192 + 2 * kQuadVT.
-// Compile-time A/B: B200 K5e2 (160 x 2 x 27) 2.50 ms vs K5e (320 x 27) 2.07
-// ms per pass -- 72 registers leave 25 warps per SM and the second chain
-// does not make up for them.  Off.
-#ifndef MP_QUAD_ILP2
-#define MP_QUAD_ILP2 0
-#endif
-#if MP_QUAD_ILP2
-#ifndef MP_QUAD2_NT
-#define MP_QUAD2_NT 320
-#endif
-constexpr int kQuad2NT = MP_QUAD2_NT;
-#endif
 // the fused pass's output tile after K3w's runs (a multiple of the round
 // tile that divides 4 x 8192)
 #ifndef MP_QUAD_TILE
@@ -237,38 +219,6 @@ constexpr int kQuad2NT = MP_QUAD2_NT;
 constexpr uint32_t kQuadTile = MP_QUAD_TILE;
 static_assert(kQuadNT * kQuadVT >= int(kQuadTile) + 2 * kQuadVT && (kQuadVT & 1),
               "K5e at the fused-pass tile");
-
-// Launch with programmatic dependent launch (mp_common.cuh pdl_*): the
-// kernel may become resident while the previous kernel of the stream drains
-// and waits for it in pdl_wait().  Opt-in (MP_PDL=1): B200 A/B, config 2
-// 0.650 vs 0.650 ms, config 4 31.16 vs 30.90 ms (the waiting CTAs of the
-// next kernel sit in the previous one's last wave).
-bool pdl_env() {
-  static const bool b = [] {
-    const char *e = std::getenv("MP_PDL");
-    return e && std::strcmp(e, "1") == 0;
-  }();
-  return b;
-}
-template <class... KArgs, class... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, uint32_t smem,
-                       cudaStream_t s, Args &&...args) {
-  if (!pdl_env()) {
-    kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
 
 template <class K> cudaError_t set_smem(K kernel, uint32_t bytes) {
   if (bytes <= 48 * 1024)
@@ -396,174 +346,14 @@ int merge_exec(const void *a, const uint32_t *av, uint64_t na, const void *b,
   constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
   auto kern = merge_tiles_kernel<KT, VALS, NT, VT, PlainMap, SINK>;
   MP_CUDA(set_smem(kern, smem));
-  MP_CUDA(launch_pdl(kern, static_cast<unsigned>(tiles), NT, smem, s, PlainMap{P, n, NV},
-                     static_cast<const T *>(a), av, static_cast<const T *>(b), bv,
-                     static_cast<T *>(out), outv, sum, uint64_t(0)));
+  kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
+      PlainMap{P, n, NV}, static_cast<const T *>(a), av, static_cast<const T *>(b), bv,
+      static_cast<T *>(out), outv, sum, 0);
   MP_LAUNCHED("merge_tiles_kernel");
   return MP_OK;
 }
 
-// ---- K1 || K2 overlap -------------------------------------------------------
-// K1 (split search) is latency-bound: dependent DRAM probes, few bytes.  K2
-// (tile merge) is HBM-bound.  Cut the tiles into chunks: the split points of
-// chunk 0 are computed on the caller's stream, those of chunks 1.. on a
-// high-priority side stream while chunk 0.. merge, so only chunk 0's search
-// latency stays on the critical path.  Fork/join by events (graph-capturable).
-constexpr int kOverlapChunks = 8;
-
-struct SideStream {
-  bool init = false;
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr;
-  cudaEvent_t ev[kOverlapChunks] = {};
-  int setup() {
-    if (init)
-      return MP_OK;
-    int least = 0, greatest = 0;
-    MP_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    MP_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest));
-    MP_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    for (auto &e : ev)
-      MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    init = true;
-    return MP_OK;
-  }
-};
-
-SideStream &side_stream() {
-  thread_local SideStream ss[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  return ss[dev & 63];
-}
-
-// split(lo, hi, stream) fills split entries [lo, hi) of E; tile(t0, t1,
-// stream) merges tiles [t0, t1) and reads entries [t0, t1] (< E).
-template <class SplitFn, class TileFn>
-int run_overlapped(uint64_t tiles, uint64_t E, SplitFn split, TileFn tile,
-                   cudaStream_t s) {
-  // Measured on B200 (round 1): the side-stream K1 chunks steal SM slots
-  // from K2 and the step got slower, so the overlap is opt-in
-  // (MP_OVERLAP_CHUNKS=2..8); the persistent SPM kernel removes K1 instead.
-  static const int env_chunks = [] {
-    const char *e = std::getenv("MP_OVERLAP_CHUNKS");
-    const int v = e ? std::atoi(e) : 1;
-    return v < 1 ? 1 : (v > kOverlapChunks ? kOverlapChunks : v);
-  }();
-  const int C = tiles >= 4096 ? env_chunks : 1;
-  if (C == 1) {
-    if (int rc = split(0, E, s))
-      return rc;
-    return tile(0, tiles, s);
-  }
-  SideStream &ss = side_stream();
-  if (int rc = ss.setup())
-    return rc;
-  uint64_t T[kOverlapChunks + 1], B[kOverlapChunks + 1];
-  for (int c = 0; c <= C; ++c) {
-    T[c] = c * tiles / C;
-    B[c] = c == 0 ? 0 : (c == C ? E : T[c] + 1);
-  }
-  if (int rc = split(B[0], B[1], s))
-    return rc;
-  MP_CUDA(cudaEventRecord(ss.fork, s));
-  MP_CUDA(cudaStreamWaitEvent(ss.side, ss.fork, 0));
-  for (int c = 1; c < C; ++c) {
-    if (int rc = split(B[c], B[c + 1], ss.side))
-      return rc;
-    MP_CUDA(cudaEventRecord(ss.ev[c], ss.side));
-  }
-  for (int c = 0; c < C; ++c) {
-    if (c > 0)
-      MP_CUDA(cudaStreamWaitEvent(s, ss.ev[c], 0));
-    if (int rc = tile(T[c], T[c + 1], s))
-      return rc;
-  }
-  return MP_OK;
-}
-
-// ---- K2s: persistent streaming SPM merge (no global split pass) ----------
-template <class KT> struct SpmShape;
-template <> struct SpmShape<KeyU32> { static constexpr int NT = 256, VT = 15, CH = 1024, SLOTS = 8; };
-template <> struct SpmShape<KeyI32> : SpmShape<KeyU32> {};
-template <> struct SpmShape<KeyF32> : SpmShape<KeyU32> {};
-template <> struct SpmShape<KeyU64> { static constexpr int NT = 256, VT = 11, CH = 512, SLOTS = 8; };
-template <> struct SpmShape<KeyI64> : SpmShape<KeyU64> {};
-template <> struct SpmShape<KeyElement> { static constexpr int NT = 256, VT = 7, CH = 256, SLOTS = 8; };
-
-template <int NT_, int VT_, int CH_, int SLOTS_> struct SpmShapeX {
-  static constexpr int NT = NT_, VT = VT_, CH = CH_, SLOTS = SLOTS_;
-};
-
-template <class KT, class Sh = SpmShape<KT>>
-int spm_merge_shape(const void *a, uint64_t na, const void *b, uint64_t nb,
-                    void *out, cudaStream_t s);
-
-// tuning hook: MP_SPM_SHAPE=1..3 selects alternative ring geometries for
-// 4-byte keys (A/B experiments); 0 = default
-template <class KT>
-int spm_merge(const void *a, uint64_t na, const void *b, uint64_t nb,
-              void *out, cudaStream_t s) {
-  static const int shape = [] {
-    const char *e = std::getenv("MP_SPM_SHAPE");
-    return e ? std::atoi(e) : 0;
-  }();
-  if constexpr (sizeof(typename KT::T) == 4) {
-    if (shape == 1)
-      return spm_merge_shape<KT, SpmShapeX<256, 15, 512, 16>>(a, na, b, nb, out, s);
-    if (shape == 2)
-      return spm_merge_shape<KT, SpmShapeX<256, 15, 1024, 16>>(a, na, b, nb, out, s);
-    if (shape == 3)
-      return spm_merge_shape<KT, SpmShapeX<512, 15, 1024, 16>>(a, na, b, nb, out, s);
-  }
-  return spm_merge_shape<KT>(a, na, b, nb, out, s);
-}
-
-template <class KT, class Sh>
-int spm_merge_shape(const void *a, uint64_t na, const void *b, uint64_t nb,
-                    void *out, cudaStream_t s) {
-  using T = typename KT::T;
-  using Cfg = SpmCfg<KT, Sh::NT, Sh::VT, Sh::CH, Sh::SLOTS>;
-  auto kern = spm_merge_kernel<KT, Sh::NT, Sh::VT, Sh::CH, Sh::SLOTS>;
-  static thread_local int grid_cache[64] = {};
-  int dev = 0;
-  MP_CUDA(cudaGetDevice(&dev));
-  int &G = grid_cache[dev & 63];
-  if (G == 0) {
-    MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(Cfg::bytes)));
-    int sms = 0, per_sm = 0;
-    MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Sh::NT + 32,
-                                                          Cfg::bytes));
-    G = sms * (per_sm > 0 ? per_sm : 1);
-  }
-  const uint64_t n = na + nb;
-  const uint64_t want = cdiv(n, 4ull * Cfg::NV);  // >= 4 windows per CTA
-  const unsigned grid = static_cast<unsigned>(want < uint64_t(G) ? want : G);
-  kern<<<grid ? grid : 1, Sh::NT + 32, Cfg::bytes, s>>>(
-      static_cast<const T *>(a), na, static_cast<const T *>(b), nb,
-      static_cast<T *>(out));
-  MP_LAUNCHED("spm_merge_kernel");
-  return MP_OK;
-}
-
-// Which engine a plain merge uses.  Default: the tile engine (K1 + K2).
-// MP_MERGE_ENGINE=spm selects the persistent streaming SPM kernel for large
-// key-only merges into a 16 B-aligned output.  Measured on B200 (round 1,
-// tools/spm_check.py): bit-exact but 2.3x slower than K1+K2 -- one CTA's
-// rings keep only ~17 KB per stream in flight, while 8 independent tile
-// CTAs per SM keep ~120 KB in flight.
-inline bool use_spm(uint64_t n, const void *out) {
-  static const bool spm = [] {
-    const char *e = std::getenv("MP_MERGE_ENGINE");
-    return e && std::strcmp(e, "spm") == 0;
-  }();
-  return spm && n >= (1ull << 20) &&
-         (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-}
-
-template <class KT, bool VALS, bool SINK, bool PEER = false>
+template <class KT, bool VALS, bool SINK>
 int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
                const uint32_t *bv, uint64_t nb, void *out, uint32_t *outv,
                unsigned long long *sum, cudaStream_t s) {
@@ -574,14 +364,12 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
   const uint64_t n = na + nb;
   if (n == 0)
     return MP_OK;
-  if (!VALS && !SINK && !PEER && use_spm(n, out))
-    return spm_merge<KT>(a, na, b, nb, out, s);
   const uint64_t tiles = cdiv(n, NV);
   if (tiles >= (1ull << 31))
     return fail(MP_ERR_INVALID, "merge too large (%llu elements)",
                 (unsigned long long)n);
-  if (!PEER && merge_fused<KT>(n)) {  // a few waves: CTAs search their own splits
-    constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
+  constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
+  if (merge_fused<KT>(n)) {  // a few waves: CTAs search their own splits
     auto kern = merge_tiles_kernel<KT, VALS, NT, VT, SearchMap, SINK>;
     MP_CUDA(set_smem(kern, smem));
     kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
@@ -594,35 +382,17 @@ int merge_impl(const void *a, const uint32_t *av, uint64_t na, const void *b,
   if (int rc = alloc_scratch(P, merge_ws_bytes<KT>(n), s))
     return rc;
   uint64_t *Pp = static_cast<uint64_t *>(P.p);
-  constexpr uint32_t smem = merge_smem_bytes<KT, VALS, NT, VT>();
-  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, PlainMap, SINK, PEER>;
+  partition_kernel<KT><<<static_cast<unsigned>(cdiv(tiles + 1, 128)), 128, 0, s>>>(
+      static_cast<const T *>(a), na, static_cast<const T *>(b), nb, NV, 0, tiles + 1, Pp,
+      nullptr);
+  MP_LAUNCHED("partition_kernel");
+  auto kern = merge_tiles_kernel<KT, VALS, NT, VT, PlainMap, SINK>;
   MP_CUDA(set_smem(kern, smem));
-  auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
-    if (hi <= lo)
-      return MP_OK;
-    partition_kernel<KT>
-        <<<static_cast<unsigned>(cdiv(hi - lo, 128)), 128, 0, st>>>(
-            static_cast<const T *>(a), na, static_cast<const T *>(b), nb, NV, 0,
-            hi, Pp, nullptr, lo);
-    MP_LAUNCHED("partition_kernel");
-    return MP_OK;
-  };
-  auto tile = [&](uint64_t t0, uint64_t t1, cudaStream_t st) -> int {
-    if (t1 <= t0)
-      return MP_OK;
-    if (t0 == 0 && t1 == tiles) {  // right behind its K1 on the same stream
-      MP_CUDA(launch_pdl(kern, static_cast<unsigned>(tiles), NT, smem, st, PlainMap{Pp, n, NV},
-                         static_cast<const T *>(a), av, static_cast<const T *>(b), bv,
-                         static_cast<T *>(out), outv, sum, uint64_t(0)));
-    } else {
-      kern<<<static_cast<unsigned>(t1 - t0), NT, smem, st>>>(
-          PlainMap{Pp, n, NV}, static_cast<const T *>(a), av,
-          static_cast<const T *>(b), bv, static_cast<T *>(out), outv, sum, t0);
-    }
-    MP_LAUNCHED("merge_tiles_kernel");
-    return MP_OK;
-  };
-  return run_overlapped(tiles, tiles + 1, split, tile, s);
+  kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
+      PlainMap{Pp, n, NV}, static_cast<const T *>(a), av, static_cast<const T *>(b), bv,
+      static_cast<T *>(out), outv, sum, 0);
+  MP_LAUNCHED("merge_tiles_kernel");
+  return MP_OK;
 }
 
 // ---- K3 + (K4 + K2) x rounds: bottom-up merge sort ---------------------------
@@ -646,33 +416,16 @@ template <class KT> SortLayout sort_layout(bool vals, uint64_t n) {
   return L;
 }
 
-// bare 32-bit keys: K3w by default (B200, 2^30 u32: block sort 7.1 ms vs
-// 9.0 ms for K3b, whole sort 31.6 vs 33.1 ms); MP_BLOCK_SORT=bare selects
-// K3b, =merge the stable K3.  (An LSD radix block sort with match.any
-// ranking was measured at 30 ms for the block pass alone and dropped.)
-int block_sort_engine() {
-  static const int e = [] {
-    const char *v = std::getenv("MP_BLOCK_SORT");
-    return !v ? 3
-              : std::strcmp(v, "merge") == 0 ? 2
-              : std::strcmp(v, "bare") == 0  ? 0
-                                             : 3;
-  }();
-  return e;
-}
-
-
-// The 16-keys-per-thread block sort: K3w (default: warp bitonic levels +
-// Merge Path passes in smem) or K3t (MP_K3W=tr: the whole bitonic network
-// in registers with smem transposes), see mp_bsort.cuh.  Same runs, same
-// bytes.  B200 (2^30 u32, ncu, current code): K3w 7.80 ms (6.1 G warp
-// instructions, ALU pipe 85 %), K3t 8.10 ms (5.3 G, ALU pipe 81 %, LSU
-// 61 %) -- both bound by the ALU pipe's min/max rate (VIMNMX issues at half
-// rate and a compare-exchange whose direction depends on the lane costs two).
-bool k3w_transposed() {
+// Block sort of bare 32-bit keys: K3w (mp_bsort.cuh, 8192-key runs) by
+// default; MP_BLOCK_SORT=merge selects the stable K3 (2048-key runs) for
+// them too (tests the generic path on bare keys).  Measured-slower
+// alternatives (K3b 4352-key runs: 33.1 vs 31.6 ms per 2^30 sort; K3t:
+// 8.44 vs 8.26 ms per block pass; an LSD radix block sort with match.any
+// ranking: 30 ms for the block pass alone) are in tools/variants/.
+bool block_sort_generic() {
   static const bool b = [] {
-    const char *v = std::getenv("MP_K3W");
-    return v && std::strcmp(v, "tr") == 0;
+    const char *v = std::getenv("MP_BLOCK_SORT");
+    return v && std::strcmp(v, "merge") == 0;
   }();
   return b;
 }
@@ -680,11 +433,7 @@ bool k3w_transposed() {
 // Run length the block sort leaves and the round tile (mp_sort's schedule).
 template <class KT, bool VALS> uint64_t sort_run0() {
   constexpr bool bare4 = !VALS && sizeof(typename KT::T) == 4 && KT::kind != kElement;
-  if (bare4 && block_sort_engine() == 0)
-    return kBareRun;
-  if (bare4 && block_sort_engine() == 3)
-    return kWarpRun;
-  return kRun;
+  return bare4 && !block_sort_generic() ? kWarpRun : kRun;
 }
 // Fused two-round passes (mp_quad.cuh) for bare 32-bit sorts whose rounds
 // are too large for the in-kernel split search: default on, MP_SORT_QUAD=0
@@ -708,8 +457,6 @@ bool sort_big_tile_env() {
 }
 template <class KT, bool VALS> uint32_t sort_round_tile() {
   const uint64_t r0 = sort_run0<KT, VALS>();
-  if (r0 == kBareRun)
-    return static_cast<uint32_t>(kBareRun);
   if (sizeof(typename KT::T) == 4 && !VALS && KT::kind != kElement && r0 % kBigTile4 == 0 &&
       sort_big_tile_env())
     return kBigTile4;
@@ -737,54 +484,27 @@ int sort_rounds_from(typename KT::T *src, uint32_t *srcv, typename KT::T *dst,
   MP_CUDA(set_smem(kern, smem));
   uint32_t tshift = static_cast<uint32_t>(__builtin_ctzll(2 * w0 / NV));  // 2w = NV << tshift
   for (uint64_t w = w0; w < n; w *= 2, ++tshift) {
-    // K4 || K2 within the round (the round's input is complete)
-    auto split = [&](uint64_t lo, uint64_t hi, cudaStream_t st) -> int {
-      if (hi <= lo)
-        return MP_OK;
-      if (lo == 0 && tiles <= k4_warp_tiles()) {
-        round_partition_warp_kernel<KT>
-            <<<static_cast<unsigned>(cdiv(hi * 32, 256)), 256, 0, st>>>(
-                src, n, w, tshift, NV, hi, P);
-        MP_LAUNCHED("round_partition_warp_kernel");
-        return MP_OK;
-      }
-      if (lo == 0 && hi == tiles) {  // right behind the previous round's K2
-        MP_CUDA(launch_pdl(round_partition_kernel<KT>, static_cast<unsigned>(cdiv(hi, 128)), 128,
-                           0, st, static_cast<const T *>(src), n, w, tshift, NV, hi, P,
-                           uint64_t(0)));
-      } else {
-        round_partition_kernel<KT>
-            <<<static_cast<unsigned>(cdiv(hi - lo, 128)), 128, 0, st>>>(
-                src, n, w, tshift, NV, hi, P, lo);
-      }
-      MP_LAUNCHED("round_partition_kernel");
-      return MP_OK;
-    };
-    auto tile = [&](uint64_t t0, uint64_t t1, cudaStream_t st) -> int {
-      if (t1 <= t0)
-        return MP_OK;
-      if (t0 == 0 && t1 == tiles) {  // right behind its K4
-        MP_CUDA(launch_pdl(kern, static_cast<unsigned>(tiles), NT, smem, st,
-                           RoundMap{P, n, w, NV, tshift}, static_cast<const T *>(src),
-                           static_cast<const uint32_t *>(srcv), static_cast<const T *>(src),
-                           static_cast<const uint32_t *>(srcv), dst, dstv,
-                           static_cast<unsigned long long *>(nullptr), uint64_t(0)));
-      } else {
-        kern<<<static_cast<unsigned>(t1 - t0), NT, smem, st>>>(
-            RoundMap{P, n, w, NV, tshift}, src, srcv, src, srcv, dst, dstv,
-            nullptr, t0);
-      }
-      MP_LAUNCHED("merge_tiles_kernel(round)");
-      return MP_OK;
-    };
     if (tiles <= merge_fuse_tiles()) {  // a few waves: CTAs search their own splits
       auto kfs = merge_tiles_kernel<KT, VALS, NT, VT, RoundSearchMap, false>;
       MP_CUDA(set_smem(kfs, smem));
       kfs<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
           RoundSearchMap{n, w, NV, tshift}, src, srcv, src, srcv, dst, dstv, nullptr, 0);
       MP_LAUNCHED("merge_tiles_kernel(round, search)");
-    } else if (int rc = run_overlapped(tiles, tiles, split, tile, s)) {
-      return rc;
+    } else {
+      // K4: pair-local split points at every tile start, then K2
+      if (tiles <= k4_warp_tiles()) {
+        round_partition_warp_kernel<KT>
+            <<<static_cast<unsigned>(cdiv(tiles * 32, 256)), 256, 0, s>>>(
+                src, n, w, tshift, NV, tiles, P);
+        MP_LAUNCHED("round_partition_warp_kernel");
+      } else {
+        round_partition_kernel<KT><<<static_cast<unsigned>(cdiv(tiles, 128)), 128, 0, s>>>(
+            src, n, w, tshift, NV, tiles, P);
+        MP_LAUNCHED("round_partition_kernel");
+      }
+      kern<<<static_cast<unsigned>(tiles), NT, smem, s>>>(
+          RoundMap{P, n, w, NV, tshift}, src, srcv, src, srcv, dst, dstv, nullptr, 0);
+      MP_LAUNCHED("merge_tiles_kernel(round)");
     }
     std::swap(src, dst);
     std::swap(srcv, dstv);
@@ -826,22 +546,18 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   uint32_t *auxv = VALS ? reinterpret_cast<uint32_t *>(ws + L.vals_off) : nullptr;
   uint64_t *P = reinterpret_cast<uint64_t *>(ws + L.part_off);
 
-  const int bs_engine = block_sort_engine();
   constexpr bool kBare4 = !VALS && sizeof(T) == 4 && KT::kind != kElement;
-  const bool use_bare = kBare4 && bs_engine == 0;
-  const bool use_warp = kBare4 && bs_engine == 3;  // K3w, kWarpRun-key runs
-  const uint64_t run0 = use_bare ? kBareRun : use_warp ? kWarpRun : kRun;
+  const bool use_warp = kBare4 && !block_sort_generic();  // K3w, kWarpRun-key runs
+  const uint64_t run0 = use_warp ? kWarpRun : kRun;
   int rounds = 0;
   for (uint64_t w = run0; w < n; w *= 2)
     ++rounds;
   // Fused round pairs: one HBM pass per two rounds (mp_quad.cuh).  B200,
-  // 2^30 u32, per pass at the 8192-output tile: K4q 0.11 + K4r 0.28 + K5e
-  // 2.07 ms (41.7 instructions per element, 320 x 27 threads) vs 2 x
-  // (1.23 + 0.06) ms for two plain rounds; with half the HBM traffic the
-  // sort also stays under the power cap: 29.0 vs 30.6 ms on one box.  Small
-  // sorts keep the plain rounds (their in-kernel split search is cheaper
-  // than K4q + K4r).
-  const int quad_mode = (use_bare || use_warp) ? sort_quad_env() : 0;
+  // 2^30 u32, per pass at the 16384-output tile: K4q 0.05 + K4r 0.13 + K5e
+  // 2.1 ms vs 2 x (1.23 + 0.06) ms for two plain rounds; with half the HBM
+  // traffic the sort also stays under the power cap.  Small sorts keep the
+  // plain rounds (their in-kernel split search is cheaper than K4q + K4r).
+  const int quad_mode = kBare4 ? sort_quad_env() : 0;
   const bool use_quad =
       quad_mode == 1 ||
       (quad_mode == 2 && cdiv(n, uint64_t(sort_round_tile<KT, VALS>())) > merge_fuse_tiles());
@@ -855,54 +571,25 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   T *dst = in_place ? aux : keys;
   uint32_t *dstv = in_place ? auxv : vals;
 
-  bool block_sorted = false;
-  if constexpr (kBare4) {
-    if (use_warp) {
+  if (use_warp) {
+    if constexpr (kBare4) {
       const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
       const uint64_t whole = al ? n / kWarpRun : 0, blocks = cdiv(n, kWarpRun);
-      auto launch = [&](auto kaligned, auto kunaligned, uint32_t smem) -> int {
-        if (whole) {
-          MP_CUDA(set_smem(kaligned, smem));
-          kaligned<<<static_cast<unsigned>(whole), kWarpNT, smem, s>>>(in, src, n, 0);
-          MP_LAUNCHED("block_sort_warp_kernel");
-        }
-        if (blocks > whole) {
-          MP_CUDA(set_smem(kunaligned, smem));
-          kunaligned<<<static_cast<unsigned>(blocks - whole), kWarpNT, smem, s>>>(in, src, n, whole);
-          MP_LAUNCHED("block_sort_warp_kernel(tail)");
-        }
-        return MP_OK;
-      };
-      const int rc = k3w_transposed()
-                         ? launch(block_sort_tr_kernel<KT, kWarpNT, true>,
-                                  block_sort_tr_kernel<KT, kWarpNT, false>,
-                                  tr_sort_smem_bytes<kWarpNT>())
-                         : launch(block_sort_warp_kernel<KT, kWarpNT, true>,
-                                  block_sort_warp_kernel<KT, kWarpNT, false>,
-                                  warp_sort_smem_bytes<kWarpNT>());
-      if (rc)
-        return rc;
-      block_sorted = true;
-    } else if (use_bare) {
-      constexpr uint32_t smem = bare_sort_smem_bytes<kBareNT, kBareVT>();
-      const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
-      const uint64_t whole = al ? n / kBareRun : 0, blocks = cdiv(n, kBareRun);
+      constexpr uint32_t smem = warp_sort_smem_bytes<kWarpNT>();
       if (whole) {
-        auto kern = block_sort_bare_kernel<KT, kBareNT, kBareVT, true>;
+        auto kern = block_sort_warp_kernel<KT, kWarpNT, true>;
         MP_CUDA(set_smem(kern, smem));
-        kern<<<static_cast<unsigned>(whole), kBareNT, smem, s>>>(in, src, n, 0);
-        MP_LAUNCHED("block_sort_bare_kernel");
+        kern<<<static_cast<unsigned>(whole), kWarpNT, smem, s>>>(in, src, n, 0);
+        MP_LAUNCHED("block_sort_warp_kernel");
       }
       if (blocks > whole) {
-        auto kern = block_sort_bare_kernel<KT, kBareNT, kBareVT, false>;
+        auto kern = block_sort_warp_kernel<KT, kWarpNT, false>;
         MP_CUDA(set_smem(kern, smem));
-        kern<<<static_cast<unsigned>(blocks - whole), kBareNT, smem, s>>>(in, src, n, whole);
-        MP_LAUNCHED("block_sort_bare_kernel(tail)");
+        kern<<<static_cast<unsigned>(blocks - whole), kWarpNT, smem, s>>>(in, src, n, whole);
+        MP_LAUNCHED("block_sort_warp_kernel(tail)");
       }
-      block_sorted = true;
     }
-  }
-  if (!block_sorted) {
+  } else {
     constexpr uint32_t smem = block_sort_smem_bytes<KT, VALS, kBlockNT, kBlockVT>();
     auto kern = block_sort_kernel<KT, VALS, kBlockNT, kBlockVT>;
     MP_CUDA(set_smem(kern, smem));
@@ -912,10 +599,8 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   }
 
   constexpr int NT = SortMergeCfg<KT>::NT, VT = SortMergeCfg<KT>::VT;
-  // round tile: TILE, or the bare block's run (4352 = 17 * 256) so that the
-  // tile divides every pair width with a power-of-two ratio
-  static_assert(NT * VT >= int(SortMergeCfg<KT>::TILE) && (2 * kRun) % SortMergeCfg<KT>::TILE == 0 &&
-                    (!kBare4 || NT * VT >= int(kBareRun)),
+  // round tile: it divides every pair width with a power-of-two ratio
+  static_assert(NT * VT >= int(SortMergeCfg<KT>::TILE) && (2 * kRun) % SortMergeCfg<KT>::TILE == 0,
                 "round tile shape");
   const uint32_t NV = sort_round_tile<KT, VALS>();
   uint64_t w = run0;
@@ -952,9 +637,8 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
         MP_LAUNCHED("quad_refine_kernel");
         return MP_OK;
       };
-      int rc = QT == kBareRun    ? launch(std::integral_constant<uint32_t, uint32_t(kBareRun)>{})
-               : QT == kQuadTile ? launch(std::integral_constant<uint32_t, kQuadTile>{})
-                                 : launch(std::integral_constant<uint32_t, 4096u>{});
+      int rc = QT == kQuadTile ? launch(std::integral_constant<uint32_t, kQuadTile>{})
+                               : launch(std::integral_constant<uint32_t, 4096u>{});
       if (rc)
         return rc;
       const uint32_t lg4w = ((4 * w) & (4 * w - 1)) == 0
@@ -963,7 +647,7 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
       auto tiles_k5 = [&](auto nt_tag) -> int {
         constexpr int QNT = decltype(nt_tag)::value;
         constexpr int QVT = QNT == kQuadNT ? kQuadVT : VT;
-        static_assert(QNT * QVT >= 4352 + 2 * QVT, "K5e: a tile's two inner merges fit the CTA");
+        static_assert(QNT * QVT >= 4096 + 2 * QVT, "K5e: a tile's two inner merges fit the CTA");
         constexpr uint32_t qsmem = quad_smem_bytes<KT, QNT, QVT>();
         auto qkern = quad_tile_kernel<KT, QNT, QVT>;
         MP_CUDA(set_smem(qkern, qsmem));
@@ -971,24 +655,8 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
         MP_LAUNCHED("quad_tile_kernel");
         return MP_OK;
       };
-#if MP_QUAD_ILP2
-      if (QT == kQuadTile) {
-        // two merge slots per thread (quad_tile2_kernel)
-        constexpr int Q2NT = kQuad2NT, Q2VT = kQuadVT;
-        static_assert(2 * Q2NT * Q2VT >= int(kQuadTile) + 2 * Q2VT, "K5e2 covers the tile");
-        constexpr uint32_t qsmem = quad2_smem_bytes<KT, Q2NT, Q2VT>();
-        auto qkern = quad_tile2_kernel<KT, Q2NT, Q2VT>;
-        MP_CUDA(set_smem(qkern, qsmem));
-        qkern<<<static_cast<unsigned>(qtiles), Q2NT, qsmem, s>>>(src, dst, n, w, lg4w, QT, QQ);
-        MP_LAUNCHED("quad_tile2_kernel");
-        rc = MP_OK;
-      } else {
-        rc = tiles_k5(std::integral_constant<int, NT>{});
-      }
-#else
       rc = QT == kQuadTile ? tiles_k5(std::integral_constant<int, kQuadNT>{})
                            : tiles_k5(std::integral_constant<int, NT>{});
-#endif
       if (rc)
         return rc;
       std::swap(src, dst);

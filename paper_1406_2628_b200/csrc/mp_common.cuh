@@ -155,64 +155,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
-// Programmatic dependent launch (PDL).  A kernel launched with the
-// programmatic-stream-serialization attribute may become resident before
-// the previous kernel in its stream has finished; pdl_wait() (griddepcontrol
-// .wait) blocks until that kernel has completed and its memory is visible,
-// and is a no-op for a normal launch.  pdl_launch_dependents() lets the next
-// such kernel launch once every CTA of this grid has started.
-__device__ __forceinline__ void pdl_wait() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-__device__ __forceinline__ void pdl_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-// MP_BULK_EVICT_FIRST (compile-time A/B): the streamed windows and tiles
-// carry an L2 evict_first policy (createpolicy + .L2::cache_hint).  B200:
-// config 2 0.650 -> 0.650/0.678 ms, config 5 5.38 -> 5.42 ms, config 4
-// 30.86 -> 30.96 ms -- no gain, off.
-#ifndef MP_BULK_EVICT_FIRST
-#define MP_BULK_EVICT_FIRST 0
-#endif
-__device__ __forceinline__ uint64_t l2_evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
 // global -> shared bulk copy completing on an mbarrier (16 B aligned, size %16)
 __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gmem_src,
                                          uint32_t bytes, uint64_t *bar) {
-#if MP_BULK_EVICT_FIRST
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
-      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first_policy())
-      : "memory");
-#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%0], [%1], %2, [%3];" ::"r"(smem_u32(smem_dst)),
       "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
-#endif
 }
 
 // shared -> global bulk copy (bulk-group completion)
 __device__ __forceinline__ void bulk_s2g(void *gmem_dst, const void *smem_src,
                                          uint32_t bytes) {
-#if MP_BULK_EVICT_FIRST
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
-                   gmem_dst),
-               "r"(smem_u32(smem_src)), "r"(bytes), "l"(l2_evict_first_policy())
-               : "memory");
-#else
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
                    gmem_dst),
                "r"(smem_u32(smem_src)), "r"(bytes)
                : "memory");
-#endif
 }
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");

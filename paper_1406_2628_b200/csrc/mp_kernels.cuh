@@ -135,7 +135,6 @@ __global__ void partition_kernel(const typename KT::T *__restrict__ a,
                                  uint64_t count, uint64_t *__restrict__ a_offs,
                                  unsigned long long *__restrict__ cmp = nullptr,
                                  uint64_t t0 = 0) {
-  pdl_launch_dependents();  // K2 may become resident while the searches run
   const uint64_t t = t0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (t >= count)
     return;
@@ -358,8 +357,6 @@ __global__ void round_partition_kernel(const typename KT::T *__restrict__ src,
                                        uint64_t tiles,
                                        uint64_t *__restrict__ P,
                                        uint64_t t0 = 0) {
-  pdl_wait();  // the round's input is the previous kernel's output
-  pdl_launch_dependents();
   const uint64_t t = t0 + blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (t >= tiles)
     return;
@@ -714,10 +711,10 @@ __device__ __forceinline__ void merge_staged_window(
   }
 }
 
-// PEER = true: the window interiors arrive through LSU vector loads instead
-// of the bulk-copy engine (used for windows in another GPU's memory).
-template <class KT, bool VALS, int NT, int VT, class Map, bool SINK = false,
-          bool PEER = false>
+// K2: one CTA per tile.  The window interiors arrive through the bulk-copy
+// engine (TMA, cp.async.bulk) on an mbarrier; windows in another GPU's
+// memory are the piece-list merge's job (mp_pieces.cuh).
+template <class KT, bool VALS, int NT, int VT, class Map, bool SINK = false>
 __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
     merge_tiles_kernel(Map map, const typename KT::T *__restrict__ a,
                        const uint32_t *__restrict__ av,
@@ -732,8 +729,6 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
   extern __shared__ __align__(128) char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
   const int tid = threadIdx.x;
-  pdl_wait();  // split points / inputs come from the previous kernel
-  pdl_launch_dependents();
 
   TileWin win;
   if constexpr (map_searches<Map>::value) {
@@ -768,19 +763,7 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
     oBv = mirror_off(oAv + na_t * 4, gBv);
   }
 
-  if constexpr (PEER) {
-    uint32_t lo;
-    uint32_t in = interior_bytes(gA, bA, &lo);
-    lsu_copy16<NT>(smem + oA + lo, gA + lo, in, tid);
-    in = interior_bytes(gB, bB, &lo);
-    lsu_copy16<NT>(smem + oB + lo, gB + lo, in, tid);
-    if constexpr (VALS) {
-      in = interior_bytes(gAv, na_t * 4, &lo);
-      lsu_copy16<NT>(smem + oAv + lo, gAv + lo, in, tid);
-      in = interior_bytes(gBv, nb_t * 4, &lo);
-      lsu_copy16<NT>(smem + oBv + lo, gBv + lo, in, tid);
-    }
-  } else if (tid == 0) {
+  if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
     uint32_t loA, loB, loAv = 0, loBv = 0;
@@ -824,8 +807,7 @@ __global__ void __launch_bounds__(NT, (merge_min_blocks<KT, VALS, NT, SINK>()))
     }
   }
   __syncthreads();
-  if constexpr (!PEER)
-    mbar_wait(bar, 0);
+  mbar_wait(bar, 0);
 
   merge_staged_window<KT, VALS, NT, VT, SINK, SENT>(smem, win, oA, oB, oAv, oBv, out, outv,
                                                     sum);

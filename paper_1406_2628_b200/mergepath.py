@@ -457,21 +457,25 @@ def segmented_parallel_merge_checksum(a, b, p: int, cache_elems: int, comp=None,
 # --------------------------------------------------------------------------
 def make_sort_plan(variant: SortVariant, n: int, cache_elems: int) -> SortPlan:
     """sort.hpp:44-55: the reference's CPU plan (block 32 or C/3).  The GPU
-    schedule (2048-key block sort + Merge Path rounds) is gpu_sort_plan()."""
+    schedule (block-sorted runs + Merge Path rounds) is gpu_sort_plan()."""
     block = SORT_BASE_RUN if variant == SortVariant.plain else _window_of(cache_elems)
     blocks = 0 if n == 0 else (n + block - 1) // block
     levels = 0 if blocks <= 1 else (blocks - 1).bit_length()
     return SortPlan(variant, block, blocks, levels)
 
 
-GPU_SORT_RUN = 2048
+GPU_SORT_RUN = 2048       # stable K3 block sort (values, 64-bit keys, element)
+GPU_SORT_RUN_BARE = 8192  # K3w block sort (bare u32 / i32 / f32 keys)
 
 
-def gpu_sort_plan(n: int) -> SortPlan:
-    """The B200 schedule: 2048-key block sort, then ceil(log2(n/2048)) rounds."""
-    blocks = 0 if n == 0 else (n + GPU_SORT_RUN - 1) // GPU_SORT_RUN
+def gpu_sort_plan(n: int, bare32: bool = False) -> SortPlan:
+    """The B200 schedule: block-sorted runs (8192 keys for bare 32-bit keys,
+    2048 otherwise), then ceil(log2(n/run)) Merge Path rounds (large bare
+    32-bit sorts run them as fused pairs: one HBM pass per two rounds)."""
+    run = GPU_SORT_RUN_BARE if bare32 else GPU_SORT_RUN
+    blocks = 0 if n == 0 else (n + run - 1) // run
     levels = 0 if blocks <= 1 else (blocks - 1).bit_length()
-    return SortPlan(SortVariant.plain, GPU_SORT_RUN, blocks, levels)
+    return SortPlan(SortVariant.plain, run, blocks, levels)
 
 
 def _sort(data, vals, key_type):

@@ -1,9 +1,10 @@
 // Minimal doctest-compatible test harness (doctest itself is not vendored in
 // the reference checkout, proj/.gitignore:2).  Implements exactly the macros
 // the reference's unit tests use -- TEST_CASE, SUBCASE, CHECK, CHECK_FALSE,
-// REQUIRE, CAPTURE, CHECK_THROWS_AS -- so tests/cpp/run_reference_tests.sh
-// can compile /root/reference/proj/tests/test_{core,parallel,sort}.cpp
-// against the drop-in headers in include/mergepath/ unchanged.
+// REQUIRE, CAPTURE, CHECK_THROWS_AS -- so the `ref_tests` target of
+// oracle/Makefile can compile /root/reference/proj/tests/
+// test_{core,parallel,sort}.cpp against the drop-in headers in
+// include/mergepath/ unchanged.
 //
 // Semantics: SUBCASE blocks run in sequence within one pass of their
 // TEST_CASE (doctest re-enters the case per subcase; the reference's

@@ -1,0 +1,306 @@
+// mp_quad_variants.cuh -- measured-slower variants taken out of the product build
+// (round 2).  Kept for reference and for A/B experiments: NOT compiled into
+// libmergepath_b200.so.  Each block is headed by what it was and the B200
+// measurement that retired it; it needs the product headers
+// (paper_1406_2628_b200/csrc/) to compile.
+#pragma once
+
+// ===== K5e fixed-step split search (MP_QUAD_FIXED_SEARCH=1): 1.35 vs 1.40 G instructions but 2.30 vs 2.07 ms =====
+// MP_QUAD_FIXED_SEARCH=1 (compile-time A/B): K5e's splits by fixed-step
+// binary lifting instead of the while loop.  B200: 1.35 vs 1.40 G
+// instructions but K5e 2.30 vs 2.07 ms (sort 30.8 vs 29.0 ms) -- every
+// warp now pays the longest chain of 13 dependent probe pairs.  Off.
+#ifndef MP_QUAD_FIXED_SEARCH
+#define MP_QUAD_FIXED_SEARCH 0
+#endif
+// Split of the smem windows A[0, na), B[0, nb) on diagonal d (core.hpp:110
+// predicate, ties to A) by binary lifting with a fixed number of steps K
+// (2^K > min(na, nb)): no loop branch, no divergence between lanes.  Probe
+// indices are clamped into the windows' neighbourhood; a clamped probe never
+// moves the answer.
+template <class KT, int K>
+__device__ __forceinline__ int split_fixed(const char *smem, uint32_t oA, int na,
+                                           uint32_t oB, int nb, int d) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  int i = d > nb ? d - nb : 0;
+  const int hi = d < na ? d : na;
+#pragma unroll
+  for (int step = 1 << (K - 1); step > 0; step >>= 1) {
+    const int j = i + step;  // does the split lie at or beyond j?
+    const int jj = j < hi ? j : hi;
+    const bool stay = take_b<KT>(lds<T>(smem, oB + (d - jj) * KS), lds<T>(smem, oA + (jj - 1) * KS));
+    i = (j <= hi && !stay) ? j : i;
+  }
+  return i;
+}
+
+
+
+// ===== K5e alternative split searches =====
+#elif MP_QUAD_FIXED_SEARCH
+    // min(na, nb) <= T / 2 <= 2^13 - 1 for tiles up to 16382 outputs
+    const int lo = split_fixed<KT, 13>(smem, oA, na, oB, nb, d1);
+#else
+    int lo = d1 > nb ? d1 - nb : 0;
+    int hi = d1 < na ? d1 : na;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (take_b<KT>(lds<T_>(smem, oB + (d1 - 1 - mid) * KS), lds<T_>(smem, oA + mid * KS)))
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+#endif
+
+
+// ===== K5e alternative split searches =====
+#elif MP_QUAD_FIXED_SEARCH
+    const int lo = split_fixed<KT, 13>(smem, oX, nx, oY, ny, d2);
+#else
+    int lo = d2 > ny ? d2 - ny : 0;
+    int hi = d2 < nx ? d2 : nx;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (take_b<KT>(lds<T_>(smem, oY + (d2 - 1 - mid) * KS), lds<T_>(smem, oX + mid * KS)))
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+#endif
+
+
+// ===== K5e2 quad_tile2_kernel (MP_QUAD_ILP2=1): two merge slots per thread; 2.50 vs 2.07 ms per pass =====
+// K5e2: K5e with two merge slots per thread.  K5e is latency-bound (B200:
+// 59 % issue, barrier and short-scoreboard stalls on top, and a fixed-step
+// search that lengthens the chains made it slower), so each thread carries
+// two independent chains: in both phases it owns slots 2t and 2t+1 (two
+// diagonals VT apart), searches them in one interleaved loop and merges them
+// back to back (the unrolled serial merges are independent, so their steps
+// interleave).  Same smem layout, sentinels and bytes as K5e.
+template <class KT, int VT>
+__device__ __forceinline__ void split2(const char *smem, uint32_t oA0, int na0, uint32_t oB0,
+                                       int nb0, int d0, bool on0, uint32_t oA1, int na1,
+                                       uint32_t oB1, int nb1, int d1, bool on1, int &r0,
+                                       int &r1) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  int lo0 = d0 > nb0 ? d0 - nb0 : 0, hi0 = on0 ? (d0 < na0 ? d0 : na0) : lo0;
+  int lo1 = d1 > nb1 ? d1 - nb1 : 0, hi1 = on1 ? (d1 < na1 ? d1 : na1) : lo1;
+  while (lo0 < hi0 || lo1 < hi1) {
+    if (lo0 < hi0) {
+      const int mid = (lo0 + hi0) >> 1;
+      if (take_b<KT>(lds<T>(smem, oB0 + (d0 - 1 - mid) * KS), lds<T>(smem, oA0 + mid * KS)))
+        hi0 = mid;
+      else
+        lo0 = mid + 1;
+    }
+    if (lo1 < hi1) {
+      const int mid = (lo1 + hi1) >> 1;
+      if (take_b<KT>(lds<T>(smem, oB1 + (d1 - 1 - mid) * KS), lds<T>(smem, oA1 + mid * KS)))
+        hi1 = mid;
+      else
+        lo1 = mid + 1;
+    }
+  }
+  r0 = lo0;
+  r1 = lo1;
+}
+
+template <class KT, int NT, int VT>
+__host__ __device__ constexpr uint32_t quad2_smem_bytes() {
+  return 64 + 2 * NT * VT * sizeof(typename KT::T) + 4 * quad_gap_bytes<KT, VT>() + 64;
+}
+
+template <class KT, int NT, int VT>
+__global__ void __launch_bounds__(NT, 800 / NT)
+    quad_tile2_kernel(const typename KT::T *__restrict__ src,
+                      typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
+                      uint32_t lg4w, uint32_t T, const QuadPt *__restrict__ Q) {
+  using T_ = typename KT::T;
+  constexpr uint32_t KS = sizeof(T_);
+  extern __shared__ __align__(128) char smem[];
+  uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+  const int tid = threadIdx.x;
+  struct Hdr {
+    uint32_t oW[4];
+    int cnt[4];
+    unsigned long long o0;
+  };
+  Hdr *hdr = reinterpret_cast<Hdr *>(smem + 16);
+  constexpr uint32_t kWin0 = 64;
+  if (tid < 32) {
+    const uint64_t t = blockIdx.x;
+    const uint64_t pos = t * T;
+    const uint64_t g = lg4w < 64 ? (pos >> lg4w) : pos / (4 * w);
+    const QuadGroup q = quad_group(g, n, w);
+    const QuadPt p0 = Q[t];
+    QuadPt p1;
+    const uint64_t gend = q.S + q.l[0] + q.l[1] + q.l[2] + q.l[3];
+    if (pos + T < gend) {
+      p1 = Q[t + 1];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        p1.i[r] = q.l[r];
+    }
+    int cnt[4];
+    const char *gW[4];
+    uint32_t oW[4];
+    uint32_t at = kWin0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      cnt[r] = static_cast<int>(p1.i[r] - p0.i[r]);
+      gW[r] = reinterpret_cast<const char *>(src + q.S + r * w + p0.i[r]);
+      oW[r] = mirror_off(at, gW[r]);
+      at = oW[r] + cnt[r] * KS + quad_gap_bytes<KT, VT>();
+    }
+    const int l = tid;
+    if (l == 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        hdr->oW[r] = oW[r];
+        hdr->cnt[r] = cnt[r];
+      }
+      hdr->o0 = pos;
+      mbar_init(bar, 1);
+      fence_mbar_init();
+      uint32_t lo[4], ib[4], tx = 0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        ib[r] = interior_bytes(gW[r], cnt[r] * KS, &lo[r]);
+        tx += ib[r];
+      }
+      mbar_arrive_expect_tx(bar, tx);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (ib[r])
+          bulk_g2s(smem + oW[r] + lo[r], gW[r] + lo[r], ib[r], bar);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if ((l >> 3) == r)
+        stage_edges<KS>(smem, oW[r], gW[r], cnt[r] * KS, l & 7);
+    if (l < VT) {
+      *reinterpret_cast<T_ *>(smem + oW[0] + (cnt[0] + l) * KS) = KT::max_key();
+      *reinterpret_cast<T_ *>(smem + oW[2] + (cnt[2] + l) * KS) = KT::max_key();
+    } else if (l == VT) {
+      *reinterpret_cast<T_ *>(smem + oW[1] + cnt[1] * KS) = KT::max_key();
+      *reinterpret_cast<T_ *>(smem + oW[3] + cnt[3] * KS) = KT::max_key();
+    }
+  }
+  __syncthreads();
+  uint32_t oW[4];
+  int cnt[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    oW[r] = hdr->oW[r];
+    cnt[r] = hdr->cnt[r];
+  }
+  const uint64_t o0 = hdr->o0;
+  const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
+  mbar_wait(bar, 0);
+
+  // ---- phase 1: slots 2t, 2t+1 of the X slots then the Y slots ----
+  T_ k0[VT], k1[VT];
+  uint32_t vals[VT];
+  const int tx = (nx + VT - 1) / VT, ty = (ny + VT - 1) / VT;
+  const int s0 = 2 * tid, s1 = 2 * tid + 1;
+  const int side0 = s0 >= tx, side1 = s1 >= tx;
+  const int u0 = s0 - side0 * tx, u1 = s1 - side1 * tx;
+  const bool on0 = side0 ? u0 < ty : true, on1 = side1 ? u1 < ty : true;
+  const uint32_t oA0 = side0 ? oW[2] : oW[0], oB0 = side0 ? oW[3] : oW[1];
+  const uint32_t oA1 = side1 ? oW[2] : oW[0], oB1 = side1 ? oW[3] : oW[1];
+  const int na0 = side0 ? cnt[2] : cnt[0], nb0 = side0 ? cnt[3] : cnt[1];
+  const int na1 = side1 ? cnt[2] : cnt[0], nb1 = side1 ? cnt[3] : cnt[1];
+  const int e0 = u0 * VT, e1 = u1 * VT;
+  {
+    int r0, r1;
+    split2<KT, VT>(smem, oA0, na0, oB0, nb0, e0, on0, oA1, na1, oB1, nb1, e1, on1, r0, r1);
+    if (on0)
+      serial_merge<KT, VT, false, true>(smem, oA0, na0, oB0, nb0, 0, 0, r0, e0 - r0, k0, vals);
+    if (on1)
+      serial_merge<KT, VT, false, true>(smem, oA1, na1, oB1, nb1, 0, 0, r1, e1 - r1, k1, vals);
+  }
+  __syncthreads();  // every window consumed
+  const uint32_t oX = oW[0], oY = oW[2];
+  auto put = [&](const T_(&k)[VT], bool on, int side, int e) {
+    if (!on)
+      return;
+    const uint32_t op = side ? oY : oX;
+    const int lim = side ? ny : nx;
+    if (e + VT <= lim) {
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        *reinterpret_cast<T_ *>(smem + op + (e + q) * KS) = k[q];
+    } else {
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        if (e + q < lim)
+          *reinterpret_cast<T_ *>(smem + op + (e + q) * KS) = k[q];
+    }
+  };
+  put(k0, on0, side0, e0);
+  put(k1, on1, side1, e1);
+  if (tid >= NT - 32) {
+    const int l = tid - (NT - 32);
+    if (l < VT)
+      *reinterpret_cast<T_ *>(smem + oX + (nx + l) * KS) = KT::max_key();
+    else if (l == VT)
+      *reinterpret_cast<T_ *>(smem + oY + ny * KS) = KT::max_key();
+  }
+  __syncthreads();
+
+  // ---- phase 2: out = merge(X, Y), diagonals 2t*VT and (2t+1)*VT ----
+  const int f0 = s0 * VT, f1 = s1 * VT;
+  const bool p0 = f0 < total, p1 = f1 < total;
+  {
+    int r0, r1;
+    split2<KT, VT>(smem, oX, nx, oY, ny, f0, p0, oX, nx, oY, ny, f1, p1, r0, r1);
+    if (p0)
+      serial_merge<KT, VT, false, true>(smem, oX, nx, oY, ny, 0, 0, r0, f0 - r0, k0, vals);
+    if (p1)
+      serial_merge<KT, VT, false, true>(smem, oX, nx, oY, ny, 0, 0, r1, f1 - r1, k1, vals);
+  }
+  __syncthreads();  // X and Y consumed
+
+  T_ *out = dst + o0;
+  const uint32_t oS = mirror_off(16, out);
+  auto stage = [&](const T_(&k)[VT], int f) {
+    if (f + VT <= total) {
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        *reinterpret_cast<T_ *>(smem + oS + (f + q) * KS) = k[q];
+    } else if (f < total) {
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        if (f + q < total)
+          *reinterpret_cast<T_ *>(smem + oS + (f + q) * KS) = k[q];
+    }
+  };
+  stage(k0, f0);
+  stage(k1, f1);
+  fence_proxy_async_smem();
+  __syncthreads();
+  uint32_t lo;
+  const uint32_t ib = interior_bytes(reinterpret_cast<const char *>(out),
+                                     static_cast<uint32_t>(total) * KS, &lo);
+  if (tid == 0 && ib) {
+    bulk_s2g(reinterpret_cast<char *>(out) + lo, smem + oS + lo, ib);
+    bulk_commit();
+  }
+  if (tid >= 32 && tid < 64) {
+    const uint32_t bytes = static_cast<uint32_t>(total) * KS;
+    const uint32_t hi = ib ? lo + ib : bytes;
+    const uint32_t hlo = ib ? lo : bytes;
+    const uint32_t nh = hlo / KS, nt = (bytes - hi) / KS;
+    const uint32_t l = tid - 32;
+    if (l < nh + nt) {
+      const uint32_t e = l < nh ? l : (hi / KS) + (l - nh);
+      out[e] = lds<T_>(smem, oS + e * KS);
+    }
+  }
+  if (tid == 0 && ib)
+    bulk_wait_read0();
+}
+

@@ -1,5 +1,9 @@
 // mp_spm.cuh -- K2s: the persistent streaming Segmented Parallel Merge.
 //
+// Taken out of the product build in round 2 (MP_MERGE_ENGINE=spm): bit-exact
+// but 2.3x slower than K1 + K2 on the B200 (one CTA's rings keep ~17 KB per
+// stream in flight vs ~120 KB for 8 tile CTAs per SM).  Not compiled.
+//
 // The paper's cache-efficient SPM (parallel.hpp:90-145)
 // mapped onto one B200 SM: a persistent CTA owns a contiguous output range
 // [D_c, D_{c+1}) (D_c = floor(c*N/G)), i.e. the reference's worker segment.
