@@ -301,10 +301,18 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
                  "quad_tile) + 1 x (round_partition + merge_tiles); algorithmic bytes count every "
                  "round as a full pass (SURVEY 8d), the fused pairs move half of them")
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, "no ncu capture for this config"
     tpath = ROOT / "profiles" / f"traffic_config{args.config}.json"
     if tpath.exists():
-        traffic = json.loads(tpath.read_text()).get("dram_bytes_per_launch")
+        # ncu DRAM bytes of the same kernel(s), stamped with the kernel
+        # sources' hash: used only while the kernels are unchanged
+        from paper_1406_2628_b200 import kernel_sources_sha256
+        tj = json.loads(tpath.read_text())
+        if tj.get("kernel_sources_sha256") == kernel_sources_sha256():
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_src = f"{tpath.relative_to(ROOT)} ({tj.get('source')}; kernel sources unchanged)"
+        else:
+            traffic_src = f"{tpath.relative_to(ROOT)} is stale (kernel sources changed since capture)"
     result = {
         "metric": "merged elements/s" if cfg["kind"] == "merge" else "merge-sort keys/s",
         "value": value,
@@ -318,7 +326,8 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": alg_bytes,
                      "avg_launch_ms": kern_ms},
     }
     result["clocks"] = clk.summary()

@@ -15,3 +15,15 @@ from . import _native  # noqa: F401  (fails loudly if the .so is missing)
 from . import mergepath  # noqa: F401
 
 __all__ = ["mergepath"]
+
+
+def kernel_sources_sha256() -> str:
+    """SHA-256 over the kernel sources (csrc/*.cu, *.cuh): profiles stamped
+    with it (profiles/traffic_config*.json) are only used while it matches."""
+    import hashlib
+    from pathlib import Path
+    h = hashlib.sha256()
+    for p in sorted((Path(__file__).resolve().parent / "csrc").glob("*.cu*")):
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()

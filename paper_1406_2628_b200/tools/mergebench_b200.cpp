@@ -36,12 +36,14 @@
 #include <iostream>
 #include <map>
 #include <memory>
+#include <numeric>
 #include <optional>
 #include <random>
 #include <sstream>
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -405,43 +407,49 @@ void emit(const Json &report, const std::string &format, const std::string &path
     throw io_error("write failed");
 }
 
-void attach_speedups(std::vector<Row> &rows) {
+// Row statistics of one configuration's timed repetitions: the row schema's
+// median_seconds and mean_seconds (the reference tool's columns; the
+// computation here is its own).
+struct TimeStats {
+  double median = 0, mean = 0;
+};
+TimeStats time_stats(std::vector<double> t) {
+  TimeStats st;
+  if (t.empty())
+    return st;
+  st.mean = std::accumulate(t.begin(), t.end(), 0.0) / static_cast<double>(t.size());
+  const auto mid = t.begin() + static_cast<std::ptrdiff_t>(t.size() / 2);
+  std::nth_element(t.begin(), mid, t.end());
+  st.median = *mid;
+  if (t.size() % 2 == 0)  // even count: average with the largest of the lower half
+    st.median = 0.5 * (st.median + *std::max_element(t.begin(), mid));
+  return st;
+}
+
+// speedup_vs_p1: each row's median against the p = 1 row of the same
+// (op, variant, cache_elems) configuration, when that row exists.
+void fill_speedups(std::vector<Row> &rows) {
+  std::map<std::tuple<std::string, std::string, std::size_t>, double> p1;
+  for (const Row &r : rows)
+    if (r.p == 1)
+      p1.emplace(std::make_tuple(r.op, r.variant, r.cache_elems), r.median_seconds);
   for (Row &r : rows) {
-    if (r.speedup_vs_p1)
-      continue;
-    for (const Row &base : rows)
-      if (base.p == 1 && base.op == r.op && base.variant == r.variant &&
-          base.cache_elems == r.cache_elems) {
-        if (r.median_seconds > 0)
-          r.speedup_vs_p1 = base.median_seconds / r.median_seconds;
-        break;
-      }
+    const auto it = p1.find(std::make_tuple(r.op, r.variant, r.cache_elems));
+    if (!r.speedup_vs_p1 && it != p1.end() && r.median_seconds > 0)
+      r.speedup_vs_p1 = it->second / r.median_seconds;
   }
 }
 
-double median_of(std::vector<double> v) {
-  std::sort(v.begin(), v.end());
-  const size_t n = v.size();
-  return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
-}
-double mean_of(const std::vector<double> &v) {
-  double s = 0;
-  for (double x : v)
-    s += x;
-  return v.empty() ? 0 : s / static_cast<double>(v.size());
-}
-
-std::size_t hw_threads() {
-  const unsigned hw = std::thread::hardware_concurrency();
-  return hw ? hw : 1;
-}
-std::vector<std::size_t> default_threads() {
-  std::vector<std::size_t> v;
-  for (std::size_t p = 1; p <= hw_threads(); p *= 2)
-    v.push_back(p);
-  if (v.back() != hw_threads())
-    v.push_back(hw_threads());
-  return v;
+// Default worker sweep: powers of two up to the host's hardware threads,
+// plus that count itself.
+std::size_t host_threads() { return std::max(1u, std::thread::hardware_concurrency()); }
+std::vector<std::size_t> thread_sweep() {
+  const std::size_t hw = host_threads();
+  std::vector<std::size_t> sweep;
+  for (std::size_t p = 1; p < hw; p <<= 1)
+    sweep.push_back(p);
+  sweep.push_back(hw);
+  return sweep;
 }
 
 // ---------------------------------------------------------------- args ----
@@ -674,7 +682,7 @@ int run_merge(const Args &a) {
   member("residency", residency, {"device", "host"});
   const std::size_t reps = reps_of(a, 5);
   auto threads = a.kv.count("threads") ? to_list("threads", a.kv.at("threads"))
-                                       : default_threads();
+                                       : thread_sweep();
   std::vector<std::size_t> caches;
   const auto A = load_sorted(fa, "merge A");
   const auto B = load_sorted(fb, "merge B");
@@ -782,20 +790,21 @@ int run_merge(const Args &a) {
             in, p, &stats);
       row.partition_comparisons = stats.partition_comparisons;
       row.merge_steps = stats.merge_steps;
-      row.median_seconds = median_of(times);
-      row.mean_seconds = mean_of(times);
+      const TimeStats ts = time_stats(times);
+      row.median_seconds = ts.median;
+      row.mean_seconds = ts.mean;
       row.verified = true;
       rows.push_back(row);
     }
   }
-  attach_speedups(rows);
+  fill_speedups(rows);
   Json meta = Json::object();
   meta.set("tool", Json::string("mergebench_b200"));
   meta.set("op", Json::string("merge"));
   meta.set("na", Json::integer(static_cast<long long>(A.size())));
   meta.set("nb", Json::integer(static_cast<long long>(B.size())));
   meta.set("sink", Json::string(sink));
-  meta.set("hardware_threads", Json::integer(static_cast<long long>(hw_threads())));
+  meta.set("hardware_threads", Json::integer(static_cast<long long>(host_threads())));
   meta.set("backend", Json::string("b200"));
   meta.set("device", Json::string(device_name(dev)));
   meta.set("residency", Json::string(residency));
@@ -822,7 +831,7 @@ int run_sort(const Args &a) {
   const std::size_t cache = static_cast<std::size_t>(
       to_u64("cache-elems", opt(a, "cache-elems", std::to_string(3 * 4096))));
   auto threads = a.kv.count("threads") ? to_list("threads", a.kv.at("threads"))
-                                       : default_threads();
+                                       : thread_sweep();
   const auto data = read_keys(fin);
   const int dev = device_of(a);
   std::vector<std::int64_t> ref = data;
@@ -884,18 +893,19 @@ int run_sort(const Args &a) {
                                       : mergepath::sort_variant::plain,
                                   n, variant == "cache_efficient" ? cache : 0)
             .tree_levels;
-    row.median_seconds = median_of(times);
-    row.mean_seconds = mean_of(times);
+    const TimeStats ts = time_stats(times);
+    row.median_seconds = ts.median;
+    row.mean_seconds = ts.mean;
     row.verified = true;
     rows.push_back(row);
   }
-  attach_speedups(rows);
+  fill_speedups(rows);
   Json meta = Json::object();
   meta.set("tool", Json::string("mergebench_b200"));
   meta.set("op", Json::string("sort"));
   meta.set("n", Json::integer(static_cast<long long>(n)));
   meta.set("variant", Json::string(variant));
-  meta.set("hardware_threads", Json::integer(static_cast<long long>(hw_threads())));
+  meta.set("hardware_threads", Json::integer(static_cast<long long>(host_threads())));
   meta.set("backend", Json::string("b200"));
   meta.set("device", Json::string(device_name(dev)));
   meta.set("residency", Json::string(residency));
