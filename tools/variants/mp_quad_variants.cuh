@@ -304,3 +304,315 @@ __global__ void __launch_bounds__(NT, 800 / NT)
     bulk_wait_read0();
 }
 
+
+
+// ===== K5p quad_persist_kernel (MP_QUAD_PERSIST, round 2): K5e as a
+// persistent, warp-specialised kernel (producer warp: split points, window
+// layout and edges one tile ahead, bulk loads/stores; NTC consumer threads:
+// K5e's two merge phases with named barriers).  B200, 2^30 u32 sort,
+// 30 steps each, 1965 MHz: K5e 27.31-27.37 ms; K5p 640x27 double-buffered
+// (1 CTA/SM, 20 consumer warps) 34.39 ms; 992x17 x2 buffers 32.98; 640x27
+// x3 buffers 33.16; 896x19 x2 32.97; 640x27 single buffer, 2 CTAs/SM
+// 33.14 (K5p 2.85 ms per pass vs K5e 2.15, issue 46.7 %).  ncu stall
+// sampling (profiles/r02/k5_stalls.md): K5e loses 55 % of its warp samples
+// at the barrier behind warp 0's per-tile setup, but the persistent form
+// cannot keep 40 consumer warps per SM with two 64 KB tile buffers each, and
+// with 20 the dependent LDS chains of the merges are exposed.  Not kept.
+// ---------------------------------------------------------------------------
+// K5p: K5e as a persistent, warp-specialised kernel.  One CTA per SM walks
+// the tiles t = blockIdx.x, + gridDim.x, ...; NBUF smem buffers hold
+// consecutive tiles.  A producer warp (the last warp) prepares tile k + NBUF
+// while NTC consumer threads merge tile k:
+//   producer: reads the tile's 4-way split points (Q[t], Q[t+1]) from HBM,
+//     lays out the four run windows in the free buffer, issues their bulk
+//     copies (TMA engine) on the buffer's `full` mbarrier, stages the
+//     unaligned window edges and the sentinels with ordinary stores; then,
+//     once the consumers have staged a tile's output (`staged` mbarrier),
+//     issues its bulk store and waits for the store to have read the
+//     buffer before refilling it;
+//   consumers: wait `full`, run K5e's two merge phases (same code, same
+//     bytes) on that buffer with named barriers among themselves only,
+//     stage the output, arrive on `staged`.
+// So the split-point loads, the window copies and the output stores of
+// neighbouring tiles overlap the merges: K5e paid a global-load latency and
+// a bulk-copy wait per tile with every thread of the CTA idle.
+// ---------------------------------------------------------------------------
+template <class KT, int NTC, int VT, int NBUF, uint32_t TT>
+struct QuadPersistCfg {
+  static constexpr uint32_t KS = sizeof(typename KT::T);
+  // one tile's four windows (TT elements) + gaps/sentinels + alignment slack
+  static constexpr uint32_t BUF = ((TT * KS + 4 * quad_gap_bytes<KT, VT>() + 256) + 127) & ~127u;
+  static constexpr uint32_t HDR = 512;  // mbarriers + per-buffer headers
+  static constexpr uint32_t bytes = HDR + NBUF * BUF;
+  static_assert(NTC * VT >= int(TT) + 2 * VT && (VT & 1) && NTC % 32 == 0, "K5p shape");
+  static_assert(NBUF * (16 + 48) + 64 <= HDR, "K5p header");
+};
+
+struct QuadHdr {
+  uint32_t oW[4];
+  int cnt[4];
+  unsigned long long o0;
+  unsigned long long pad;
+};
+
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+template <class KT, int NTC, int VT, int NBUF, uint32_t TT>
+__global__ void __launch_bounds__(NTC + 32, NBUF == 1 ? 2 : 1)
+    quad_persist_kernel(const typename KT::T *__restrict__ src,
+                        typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
+                        uint32_t lg4w, const QuadPt *__restrict__ Q, uint64_t tiles) {
+  using T_ = typename KT::T;
+  using Cfg = QuadPersistCfg<KT, NTC, VT, NBUF, TT>;
+  constexpr uint32_t KS = sizeof(T_);
+  extern __shared__ __align__(128) char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+  uint64_t *staged = full + NBUF;
+  QuadHdr *hdr = reinterpret_cast<QuadHdr *>(smem + 64);
+  auto buf = [&](int b) { return smem + Cfg::HDR + b * Cfg::BUF; };
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(full + b, 1);
+      mbar_init(staged + b, 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  constexpr uint32_t kWin0 = 64;
+
+  if (tid >= NTC) {  // ---------------- producer warp ----------------
+    const int l = tid - NTC;
+    // Everything about tile t that needs HBM round trips -- its split
+    // points, window layout and the unaligned window edges (lane l holds
+    // edge element l & 7 of window l >> 3) -- is read one tile ahead, while
+    // the consumers merge; filling a buffer then only waits for the buffer.
+    struct Prep {
+      uint64_t pos;
+      const char *gW[4];
+      uint32_t oW[4];
+      int cnt[4];
+      T_ edge;
+      uint32_t edge_off;  // byte offset in the buffer (~0u: none)
+    };
+    auto prepare = [&](uint64_t t) {
+      Prep p;
+      p.pos = t * TT;
+      const uint64_t g = p.pos >> lg4w;
+      const QuadGroup q = quad_group(g, n, w);
+      const QuadPt p0 = Q[t];
+      QuadPt p1;
+      const uint64_t gend = q.S + q.l[0] + q.l[1] + q.l[2] + q.l[3];
+      if (p.pos + TT < gend) {
+        p1 = Q[t + 1];
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          p1.i[r] = q.l[r];
+      }
+      uint32_t at = kWin0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        p.cnt[r] = static_cast<int>(p1.i[r] - p0.i[r]);
+        p.gW[r] = reinterpret_cast<const char *>(src + q.S + r * w + p0.i[r]);
+        p.oW[r] = mirror_off(at, p.gW[r]);
+        at = p.oW[r] + p.cnt[r] * KS + quad_gap_bytes<KT, VT>();
+      }
+      // this lane's edge element (stage_edges' split, as a load now and a
+      // store at fill time): heads [0, lo) and tails [hi, bytes) < 32 B
+      const int r = l >> 3, e = l & 7;
+      const uintptr_t s0 = reinterpret_cast<uintptr_t>(p.gW[r]);
+      const uint32_t bytes = p.cnt[r] * KS;
+      const uintptr_t is = (s0 + 15) & ~uintptr_t(15);
+      const uintptr_t ie = (s0 + bytes) & ~uintptr_t(15);
+      const uint32_t lo = ie > is ? static_cast<uint32_t>(is - s0) : bytes;
+      const uint32_t hi = ie > is ? static_cast<uint32_t>(ie - s0) : bytes;
+      const uint32_t nh = lo / KS, nt = (bytes - hi) / KS;
+      p.edge_off = ~0u;
+      if (static_cast<uint32_t>(e) < nh + nt) {
+        const uint32_t o = static_cast<uint32_t>(e) < nh ? e * KS : hi + (e - nh) * KS;
+        p.edge = *reinterpret_cast<const T_ *>(p.gW[r] + o);
+        p.edge_off = p.oW[r] + o;
+      }
+      return p;
+    };
+    auto fill = [&](const Prep &p, int b) {
+      char *base = buf(b);
+      if (p.edge_off != ~0u)
+        *reinterpret_cast<T_ *>(base + p.edge_off) = p.edge;
+      if (l < VT) {  // sentinels behind the windows (outside the bulk copies)
+        *reinterpret_cast<T_ *>(base + p.oW[0] + (p.cnt[0] + l) * KS) = KT::max_key();
+        *reinterpret_cast<T_ *>(base + p.oW[2] + (p.cnt[2] + l) * KS) = KT::max_key();
+      } else if (l == VT) {
+        *reinterpret_cast<T_ *>(base + p.oW[1] + p.cnt[1] * KS) = KT::max_key();
+        *reinterpret_cast<T_ *>(base + p.oW[3] + p.cnt[3] * KS) = KT::max_key();
+      }
+      if (l == 0) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          hdr[b].oW[r] = p.oW[r];
+          hdr[b].cnt[r] = p.cnt[r];
+        }
+        hdr[b].o0 = p.pos;
+      }
+      __syncwarp();
+      if (l == 0) {
+        uint32_t lo[4], ib[4], tx = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          ib[r] = interior_bytes(p.gW[r], p.cnt[r] * KS, &lo[r]);
+          tx += ib[r];
+        }
+        mbar_arrive_expect_tx(full + b, tx);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (ib[r])
+            bulk_g2s(base + p.oW[r] + lo[r], p.gW[r] + lo[r], ib[r], full + b);
+      }
+    };
+    // issue the bulk store of the tile staged in buffer b (lane 0), then
+    // wait until the store has read the buffer
+    auto store_out = [&](int b) {
+      char *base = buf(b);
+      const QuadHdr &h = hdr[b];
+      const int total = h.cnt[0] + h.cnt[1] + h.cnt[2] + h.cnt[3];
+      T_ *out = dst + h.o0;
+      const uint32_t oS = mirror_off(16, out);
+      uint32_t lo;
+      const uint32_t ib = interior_bytes(reinterpret_cast<const char *>(out),
+                                         static_cast<uint32_t>(total) * KS, &lo);
+      if (l == 0 && ib) {
+        bulk_s2g(reinterpret_cast<char *>(out) + lo, base + oS + lo, ib);
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      __syncwarp();
+    };
+    uint64_t k = 0;
+    uint64_t t = blockIdx.x;
+    if (t < tiles) {
+      Prep next = prepare(t);
+      for (; t < tiles; t += gridDim.x, ++k) {
+        const Prep cur = next;
+        const int b = static_cast<int>(k % NBUF);
+        const uint32_t use = static_cast<uint32_t>(k / NBUF);
+        if (t + gridDim.x < tiles)  // tile k + 1's HBM round trips, now
+          next = prepare(t + gridDim.x);
+        if (k >= NBUF) {  // buffer b still holds tile k - NBUF: store it first
+          mbar_wait(staged + b, (use - 1) & 1);
+          store_out(b);
+        }
+        fill(cur, b);
+      }
+    }
+    // drain: the last min(k, NBUF) tiles' outputs
+    for (uint64_t j = k > NBUF ? k - NBUF : 0; j < k; ++j) {
+      const int b = static_cast<int>(j % NBUF);
+      mbar_wait(staged + b, static_cast<uint32_t>(j / NBUF) & 1);
+      store_out(b);
+    }
+    if (l == 0)
+      bulk_wait0();  // the stores' global writes complete before the CTA exits
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  uint64_t k = 0;
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++k) {
+    const int b = static_cast<int>(k % NBUF);
+    mbar_wait(full + b, static_cast<uint32_t>(k / NBUF) & 1);
+    const char *base = buf(b);
+    char *wbase = buf(b);
+    uint32_t oW[4];
+    int cnt[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      oW[r] = hdr[b].oW[r];
+      cnt[r] = hdr[b].cnt[r];
+    }
+    const uint64_t o0 = hdr[b].o0;
+    const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
+
+    // phase 1: X = merge(R0w, R1w), Y = merge(R2w, R3w) (threads dealt by size)
+    T_ keys[VT];
+    uint32_t vals[VT];
+    const int tx = (nx + VT - 1) / VT;
+    const int side = tid >= tx ? 1 : 0;
+    const int t1 = tid - side * tx;
+    const uint32_t oA = side ? oW[2] : oW[0], oB = side ? oW[3] : oW[1];
+    const int na = side ? cnt[2] : cnt[0], nb = side ? cnt[3] : cnt[1];
+    const int d1 = t1 * VT;
+    const bool act1 = d1 < na + nb;
+    if (act1) {
+      const int lo = split_predicted<KT, MP_QUAD_PRED_LOGW>(
+          base, oA, na, oB, nb, d1, static_cast<float>(na) / static_cast<float>(na + nb));
+      serial_merge<KT, VT, false, true>(base, oA, na, oB, nb, 0, 0, lo, d1 - lo, keys, vals);
+    }
+    consumer_sync(NTC);  // every window consumed
+    const uint32_t oX = oW[0], oY = oW[2];
+    if (act1) {
+      const uint32_t op = side ? oY : oX;
+      const int lim = side ? ny : nx;
+      if (d1 + VT <= lim) {
+#pragma unroll
+        for (int e = 0; e < VT; ++e)
+          *reinterpret_cast<T_ *>(wbase + op + (d1 + e) * KS) = keys[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < VT; ++e)
+          if (d1 + e < lim)
+            *reinterpret_cast<T_ *>(wbase + op + (d1 + e) * KS) = keys[e];
+      }
+    }
+    if (tid >= NTC - 32) {  // the last consumer warp: X's VT sentinels and Y's one
+      const int l = tid - (NTC - 32);
+      if (l < VT)
+        *reinterpret_cast<T_ *>(wbase + oX + (nx + l) * KS) = KT::max_key();
+      else if (l == VT)
+        *reinterpret_cast<T_ *>(wbase + oY + ny * KS) = KT::max_key();
+    }
+    consumer_sync(NTC);
+
+    // phase 2: out = merge(X, Y), ties to X
+    const int d2 = tid * VT;
+    if (d2 < total) {
+      const int lo = split_predicted<KT, MP_QUAD_PRED_LOGW>(
+          base, oX, nx, oY, ny, d2, static_cast<float>(nx) / static_cast<float>(total));
+      serial_merge<KT, VT, false, true>(base, oX, nx, oY, ny, 0, 0, lo, d2 - lo, keys, vals);
+    }
+    consumer_sync(NTC);  // X and Y consumed
+
+    T_ *out = dst + o0;
+    const uint32_t oS = mirror_off(16, out);
+    // the 16 B-aligned interior goes out through the producer's bulk store;
+    // the < 16 B head [0, h_end) and tail [t_beg, total) straight from the
+    // registers of the threads that own them (nothing reads the buffer
+    // after `staged`)
+    uint32_t olo;
+    const uint32_t oib = interior_bytes(reinterpret_cast<const char *>(out),
+                                        static_cast<uint32_t>(total) * KS, &olo);
+    const int h_end = oib ? static_cast<int>(olo / KS) : total;
+    const int t_beg = oib ? static_cast<int>((olo + oib) / KS) : total;
+    if (d2 >= h_end && d2 + VT <= t_beg) {
+#pragma unroll
+      for (int e = 0; e < VT; ++e)
+        *reinterpret_cast<T_ *>(wbase + oS + (d2 + e) * KS) = keys[e];
+    } else if (d2 < total) {
+#pragma unroll
+      for (int e = 0; e < VT; ++e) {
+        const int x = d2 + e;
+        if (x < h_end || (x >= t_beg && x < total))
+          out[x] = keys[e];
+        else if (x < total)
+          *reinterpret_cast<T_ *>(wbase + oS + x * KS) = keys[e];
+      }
+    }
+    fence_proxy_async_smem();
+    consumer_sync(NTC);
+    if (tid == 0)
+      mbar_arrive(staged + b);
+  }
+}
+
