@@ -390,12 +390,44 @@ def run_e2e(args, cfg, torch, N, dev, local, dist_on, ws):
             call()
         el = time.perf_counter() - t
         barrier(dist_on)
+        # the same call on pageable memory (numpy arrays: what a std::vector
+        # caller of the drop-in passes): staged through pinned slots
+        pg = None
+        if not dist_on:
+            if cfg["kind"] == "merge":
+                pa_, pb_ = ha.numpy().copy(), hb.numpy().copy()
+                po_ = np.empty_like(hout.numpy())
+                pav = hav.numpy().copy() if hav is not None else None
+                pbv = hbv.numpy().copy() if hbv is not None else None
+                pov = np.empty_like(houtv.numpy()) if houtv is not None else None
+                q = (lambda x: x.ctypes.data if x is not None else None)
+
+                def pcall():
+                    N.check(N.lib.mp_merge_host(kt, q(pa_), q(pav), len(pa_), q(pb_), q(pbv),
+                                                len(pb_), q(po_), q(pov), local))
+            else:
+                px_ = hx.numpy().copy()
+                po_ = np.empty_like(px_)
+
+                def pcall():
+                    N.check(N.lib.mp_sort_host(kt, px_.ctypes.data, None, n, po_.ctypes.data,
+                                               None, local))
+            pcall()
+            psteps = max(1, min(steps, 3))
+            t = time.perf_counter()
+            for _ in range(psteps):
+                pcall()
+            pel = time.perf_counter() - t
+            pg = {"value": n * psteps / pel, "steps": psteps,
+                  "note": "same call on pageable host arrays (staged through pinned slots)"}
     el = max_over_ranks(el, dist_on)
     unit = "elements/s" if cfg["kind"] == "merge" else "keys/s"
     del np
     return {"value": n * ws * steps / el, "unit": unit, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps,
             "api": "mp_merge_host" if cfg["kind"] == "merge" else "mp_sort_host",
+            "memory": "pinned",
+            **({"pageable": pg} if pg else {}),
             **({"sample": sample} if cfg["kind"] == "merge" and sample else {})}
 
 

@@ -142,7 +142,11 @@ int mp_segment_plan(int key_type, const void *a, uint64_t na, const void *b,
 
 /* ---- host-buffer entry points (synchronous) --------------------------- */
 /* Counters (`comparisons`, `*_comparisons`) are host uint64 here, may be
- * NULL, and accumulate (+=) like the reference's stats pointers. */
+ * NULL, and accumulate (+=) like the reference's stats pointers.
+ * mp_merge_host / mp_sort_host stream chunks over PCIe (H2D, kernels, D2H
+ * overlapped on three streams).  Page-locked buffers are DMA'd directly;
+ * pageable ones (a plain std::vector) are staged chunk by chunk through
+ * pinned slots by a pool of host threads, overlapped with the transfers. */
 int mp_partition_host(int key_type, const void *a, uint64_t na, const void *b,
                       uint64_t nb, uint64_t p, uint64_t *a_offs,
                       uint64_t *comparisons, int device);
@@ -258,8 +262,13 @@ int mp_wait(const uint64_t *flag, uint64_t value, void *stream);
 /* ---- memory ------------------------------------------------------------ */
 /* Scratch comes from a library-private stream-ordered pool per device that
  * keeps its memory between calls; mp_release(device) waits for the device,
- * frees the host-pipeline slot buffers and trims that pool to zero. */
+ * frees the host-pipeline slot buffers (device slots and the pinned staging
+ * slots of pageable host calls) and trims that pool to zero. */
 int mp_release(int device);
+/* Page-locked host memory (cudaHostAlloc, portable across devices): host
+ * buffers the DMA engines read directly.  NULL on failure. */
+void *mp_host_alloc(uint64_t bytes);
+int mp_host_free(void *p);
 
 /* ---- synthetic inputs (bench/tests; SURVEY.md §8d generator) ---------- */
 /* out[k] = config key kind `gen_kind` at global index first+k for `seed`:

@@ -65,6 +65,8 @@ SIGNATURES = [
     ("mp_ipc_close", _i, [_p]),
     ("mp_ipc_open_count", _u64, []),
     ("mp_release", _i, [_i]),
+    ("mp_host_alloc", _p, [_u64]),
+    ("mp_host_free", _i, [_p]),
     ("mp_signal", _i, [_p, _u64, _p]),
     ("mp_wait", _i, [_p, _u64, _p]),
     ("mp_generate", _i, [_i, _u64, _u64, _u64, _p, _p]),

@@ -17,7 +17,10 @@
 #include "../../include/mergepath_b200.h"
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cstdlib>
+#include <thread>
+#include <tuple>
 #include <vector>
 
 #include "mp_kernels.cuh"
@@ -1023,6 +1026,135 @@ cudaStream_t host_stream(int device) {
 
 
 // ---------------------------------------------------------------------------
+// Pageable host spans.  The drop-in's natural callers hand over std::vector
+// memory, which the DMA engines cannot read: the driver then stages it at
+// ~11 GB/s.  Instead, the host pipelines below stage pageable chunks
+// through pinned buffers with a pool of host threads (memcpy at the host's
+// memory bandwidth, ~70-80 GB/s on the B200 box, tools/host_copy_probe.py)
+// while the copy engines and the SMs work on neighbouring chunks.
+// ---------------------------------------------------------------------------
+bool is_pageable(const void *p) {
+  if (!p)
+    return false;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
+
+// Blocking parallel memcpy over persistent worker threads.
+class CopyPool {
+ public:
+  static CopyPool &get() {
+    static CopyPool pool;
+    return pool;
+  }
+  // copy every (dst, src, bytes) job, each split into pieces over the threads
+  void copy(const std::vector<std::tuple<void *, const void *, size_t>> &jobs) {
+    std::lock_guard<std::mutex> call(call_mu_);
+    size_t total = 0;
+    for (const auto &j : jobs)
+      total += std::get<2>(j);
+    if (!total)
+      return;
+    // pieces of >= 1 MiB, at most one per thread and job
+    std::vector<Part> parts;
+    for (const auto &j : jobs) {
+      const size_t bytes = std::get<2>(j);
+      if (!bytes)
+        continue;
+      const size_t k = std::max<size_t>(
+          1, std::min<size_t>(nthreads_ + 1, bytes >> 20));
+      for (size_t q = 0; q < k; ++q) {
+        const size_t lo = q * bytes / k, hi = (q + 1) * bytes / k;
+        parts.push_back({static_cast<char *>(std::get<0>(j)) + lo,
+                         static_cast<const char *>(std::get<1>(j)) + lo, hi - lo});
+      }
+    }
+    {
+      // the part list changes only while no worker is inside work()
+      std::unique_lock<std::mutex> lk(mu_);
+      idle_cv_.wait(lk, [&] { return active_ == 0; });
+      parts_.swap(parts);
+      next_.store(0);
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == parts_.size(); });
+  }
+
+ private:
+  struct Part {
+    char *dst;
+    const char *src;
+    size_t bytes;
+  };
+  CopyPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    nthreads_ = std::min<unsigned>(hw > 1 ? hw - 1 : 1, 15);
+    for (unsigned t = 0; t < nthreads_; ++t)
+      threads_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto &t : threads_)
+      t.join();
+  }
+  void work() {
+    size_t finished = 0;
+    for (size_t i = next_.fetch_add(1); i < parts_.size(); i = next_.fetch_add(1)) {
+      std::memcpy(parts_[i].dst, parts_[i].src, parts_[i].bytes);
+      ++finished;
+    }
+    if (finished) {
+      std::lock_guard<std::mutex> lk(mu_);
+      done_ += finished;
+      if (done_ == parts_.size())
+        done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_)
+          return;
+        ++active_;
+      }
+      work();
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--active_ == 0)
+          idle_cv_.notify_all();
+      }
+    }
+  }
+  unsigned nthreads_ = 1;
+  std::vector<std::thread> threads_;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_, idle_cv_;
+  std::vector<Part> parts_;
+  unsigned active_ = 0;
+  std::atomic<size_t> next_{0};
+  size_t done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// ---------------------------------------------------------------------------
 // Host-buffer merge, pipelined over PCIe.
 //
 // The output is cut into chunks of Q elements at host-side Merge Path splits
@@ -1034,6 +1166,8 @@ cudaStream_t host_stream(int device) {
 // max(H2D bytes, D2H bytes) / PCIe bandwidth instead of their sum.
 // ---------------------------------------------------------------------------
 constexpr int kSlots = 4;
+constexpr uint64_t kDrainLag = 2;  // pageable outputs: chunks in flight before a drain
+static_assert(kSlots > int(kDrainLag), "a drained slot is free before its next D2H");
 
 struct HostPipe {
   std::mutex mu;  // one host call per device at a time
@@ -1042,6 +1176,9 @@ struct HostPipe {
   cudaEvent_t ev_h2d[kSlots] = {}, ev_cmp[kSlots] = {}, ev_d2h[kSlots] = {};
   void *buf = nullptr;
   size_t buf_bytes = 0;
+  // pinned host staging for pageable callers: kSlots slots in and out
+  void *pin = nullptr;
+  size_t pin_bytes = 0;
 
   int setup() {
     if (init)
@@ -1067,6 +1204,18 @@ struct HostPipe {
     }
     MP_CUDA(cudaMalloc(&buf, bytes));
     buf_bytes = bytes;
+    return MP_OK;
+  }
+  int reserve_pinned(size_t bytes) {
+    if (bytes <= pin_bytes)
+      return MP_OK;
+    if (pin) {
+      cudaFreeHost(pin);
+      pin = nullptr;
+      pin_bytes = 0;
+    }
+    MP_CUDA(cudaHostAlloc(&pin, bytes, cudaHostAllocDefault));
+    pin_bytes = bytes;
     return MP_OK;
   }
 };
@@ -1159,44 +1308,97 @@ int merge_host_pipelined(const void *a_, const uint32_t *av, uint64_t na,
   const uint64_t slot_bytes = o_ws + up(merge_ws_bytes<KT>(Q));
   if (int rc = P.reserve(slot_bytes * kSlots))
     return rc;
+  // Pageable spans are staged through pinned host slots (CopyPool): chunk
+  // k's inputs are copied into pinned slot k % kSlots before its H2D copies
+  // are issued, and its output is copied out of the pinned slot after its
+  // D2H copy landed -- one chunk later, so the copy engines and the merge
+  // of chunk k overlap the host copies of chunks k - 1 and k + 1.
+  const bool stage_in = is_pageable(a) || is_pageable(b) ||
+                        (VALS && (is_pageable(av) || is_pageable(bv)));
+  const bool stage_out = is_pageable(out) || (VALS && is_pageable(outv));
+  // pinned slot layout: widened A, B (+ values) ranges, then the output
+  const uint64_t pi_a = 0, pi_b = up(QA * ks) + kAlign;
+  const uint64_t pi_av = pi_b + up(QA * ks) + kAlign;
+  const uint64_t pi_bv = pi_av + (VALS ? up(QA * 4) + kAlign : 0);
+  const uint64_t pi_o = pi_bv + (VALS ? up(QA * 4) + kAlign : 0);
+  const uint64_t pi_ov = pi_o + up(Q * ks);
+  const uint64_t pin_slot = (pi_ov + (VALS ? up(Q * 4) : 0) + kAlign - 1) & ~(kAlign - 1);
+  if (stage_in || stage_out)
+    if (int rc = P.reserve_pinned(pin_slot * kSlots))
+      return rc;
+  std::vector<std::tuple<void *, const void *, size_t>> jobs;
+  auto drain = [&](uint64_t j) -> int {  // chunk j's output: pinned -> caller
+    const int sj = static_cast<int>(j % kSlots);
+    const char *pin = static_cast<const char *>(P.pin) + sj * pin_slot;
+    MP_CUDA(cudaEventSynchronize(P.ev_d2h[sj]));
+    const uint64_t e0 = bounds[j], e1 = bounds[j + 1];
+    jobs.clear();
+    jobs.emplace_back(out + e0, pin + pi_o, (e1 - e0) * ks);
+    if (VALS)
+      jobs.emplace_back(outv + e0, pin + pi_ov, (e1 - e0) * 4);
+    CopyPool::get().copy(jobs);
+    return MP_OK;
+  };
+  // [lo, lo + cnt) of a host array widened to 4 KiB boundaries (clamped to
+  // the array, whole elements): {first byte, bytes, element shift of lo}
+  struct Span {
+    uintptr_t wb;
+    uint64_t bytes;
+    int64_t shift;
+  };
+  auto widen = [&](const void *src, uint64_t lo, uint64_t cnt, uint64_t total,
+                   uint64_t es) -> Span {
+    if (!cnt)
+      return {0, 0, 0};
+    const uintptr_t s0 = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t beg = s0 + lo * es, end = s0 + (lo + cnt) * es;
+    uintptr_t wb = beg & ~uintptr_t(kAlign - 1);
+    uintptr_t we = (end + kAlign - 1) & ~uintptr_t(kAlign - 1);
+    wb = wb < s0 ? s0 + ((beg - s0) % es) : wb;
+    wb = beg - ((beg - wb) / es) * es;  // whole elements before lo
+    we = we > s0 + total * es ? s0 + total * es : we;
+    we = end + ((we - end) / es) * es;
+    return {wb, we - wb, static_cast<int64_t>((beg - wb) / es)};
+  };
   uint64_t a_lo = 0;  // split of chunk k's start
   for (uint64_t k = 0; k < chunks; ++k) {
     const int s = static_cast<int>(k % kSlots);
     char *base = static_cast<char *>(P.buf) + s * slot_bytes;
+    char *pin = (stage_in || stage_out) ? static_cast<char *>(P.pin) + s * pin_slot : nullptr;
     const uint64_t d0 = bounds[k], d1 = bounds[k + 1];
     const uint64_t a_hi = d1 == n ? na : host_diag_search<KT>(a, na, b, nb, d1);
     const uint64_t ca = a_hi - a_lo, cb = (d1 - a_hi) - (d0 - a_lo);
     const uint64_t b_lo = d0 - a_lo;
     if (k >= kSlots)  // the slot's previous chunk has left the device
       MP_CUDA(cudaStreamWaitEvent(P.h2d, P.ev_d2h[s], 0));
-    // widen [lo, lo + cnt) of a host array to 4 KiB boundaries (clamped to
-    // the array); returns the element shift of `lo` inside the copy
-    auto h2d = [&](char *dst, const void *src, uint64_t lo, uint64_t cnt,
-                   uint64_t total, uint64_t es) -> int64_t {
-      if (!cnt)
-        return 0;
-      const uintptr_t s0 = reinterpret_cast<uintptr_t>(src);
-      const uintptr_t beg = s0 + lo * es, end = s0 + (lo + cnt) * es;
-      uintptr_t wb = beg & ~uintptr_t(kAlign - 1);
-      uintptr_t we = (end + kAlign - 1) & ~uintptr_t(kAlign - 1);
-      wb = wb < s0 ? s0 + ((beg - s0) % es) : wb;
-      wb = beg - ((beg - wb) / es) * es;  // whole elements before lo
-      we = we > s0 + total * es ? s0 + total * es : we;
-      we = end + ((we - end) / es) * es;
-      if (cudaMemcpyAsync(dst, reinterpret_cast<const void *>(wb), we - wb,
-                          cudaMemcpyHostToDevice, P.h2d) != cudaSuccess)
-        return -1;
-      return static_cast<int64_t>((beg - wb) / es);
-    };
-    const int64_t sa = h2d(base + o_a, a, a_lo, ca, na, ks);
-    const int64_t sb = h2d(base + o_b, b, b_lo, cb, nb, ks);
-    int64_t sav = 0, sbv = 0;
-    if (VALS) {
-      sav = h2d(base + o_av, av, a_lo, ca, na, 4);
-      sbv = h2d(base + o_bv, bv, b_lo, cb, nb, 4);
+    const Span spans[4] = {widen(a, a_lo, ca, na, ks), widen(b, b_lo, cb, nb, ks),
+                           VALS ? widen(av, a_lo, ca, na, 4) : Span{0, 0, 0},
+                           VALS ? widen(bv, b_lo, cb, nb, 4) : Span{0, 0, 0}};
+    const uint64_t dev_off[4] = {o_a, o_b, o_av, o_bv};
+    const uint64_t pin_off[4] = {pi_a, pi_b, pi_av, pi_bv};
+    const void *from[4];
+    if (stage_in) {
+      if (k >= kSlots)  // the slot's pinned inputs were last read by chunk k - kSlots
+        MP_CUDA(cudaEventSynchronize(P.ev_h2d[s]));
+      jobs.clear();
+      for (int r = 0; r < 4; ++r) {
+        // pinned copy at the same offset mod 4 KiB (page-aligned DMA source)
+        char *p = pin + pin_off[r] + (spans[r].wb & (kAlign - 1));
+        from[r] = p;
+        if (spans[r].bytes)
+          jobs.emplace_back(p, reinterpret_cast<const void *>(spans[r].wb), spans[r].bytes);
+      }
+      CopyPool::get().copy(jobs);
+    } else {
+      for (int r = 0; r < 4; ++r)
+        from[r] = reinterpret_cast<const void *>(spans[r].wb);
     }
-    if (sa < 0 || sb < 0 || sav < 0 || sbv < 0)
-      return cuda_fail(cudaGetLastError(), "host pipeline H2D copy");
+    for (int r = 0; r < (VALS ? 4 : 2); ++r)
+      if (spans[r].bytes)
+        MP_CUDA(cudaMemcpyAsync(base + dev_off[r], from[r], spans[r].bytes,
+                                cudaMemcpyHostToDevice, P.h2d));
+    const int64_t sa = spans[0].shift, sb = spans[1].shift;
+    const int64_t sav = spans[2].shift, sbv = spans[3].shift;
     MP_CUDA(cudaEventRecord(P.ev_h2d[s], P.h2d));
     MP_CUDA(cudaStreamWaitEvent(P.cmp, P.ev_h2d[s], 0));
     uint64_t *ws = reinterpret_cast<uint64_t *>(base + o_ws);
@@ -1213,14 +1415,24 @@ int merge_host_pipelined(const void *a_, const uint32_t *av, uint64_t na,
       return rc;
     MP_CUDA(cudaEventRecord(P.ev_cmp[s], P.cmp));
     MP_CUDA(cudaStreamWaitEvent(P.d2h, P.ev_cmp[s], 0));
-    MP_CUDA(cudaMemcpyAsync(out + d0, base + o_o, (d1 - d0) * ks,
-                            cudaMemcpyDeviceToHost, P.d2h));
-    if (VALS)
-      MP_CUDA(cudaMemcpyAsync(outv + d0, base + o_ov, (d1 - d0) * 4,
-                              cudaMemcpyDeviceToHost, P.d2h));
+    void *to = stage_out ? static_cast<void *>(pin + pi_o) : static_cast<void *>(out + d0);
+    MP_CUDA(cudaMemcpyAsync(to, base + o_o, (d1 - d0) * ks, cudaMemcpyDeviceToHost, P.d2h));
+    if (VALS) {
+      void *tov = stage_out ? static_cast<void *>(pin + pi_ov) : static_cast<void *>(outv + d0);
+      MP_CUDA(cudaMemcpyAsync(tov, base + o_ov, (d1 - d0) * 4, cudaMemcpyDeviceToHost, P.d2h));
+    }
     MP_CUDA(cudaEventRecord(P.ev_d2h[s], P.d2h));
+    // drain two chunks behind: chunk k - 2's D2H has landed by now, so the
+    // host never waits on the copy engines (kSlots >= 3 keeps k's slot free)
+    if (stage_out && k >= kDrainLag)
+      if (int rc = drain(k - kDrainLag))
+        return rc;
     a_lo = a_hi;
   }
+  if (stage_out)
+    for (uint64_t j = chunks > kDrainLag ? chunks - kDrainLag : 0; j < chunks; ++j)
+      if (int rc = drain(j))
+        return rc;
   MP_CUDA(cudaStreamSynchronize(P.d2h));
   return MP_OK;
 }
@@ -1820,12 +2032,33 @@ int sort_host_pipelined(const void *keys_, const uint32_t *vals, uint64_t n,
   uint64_t *P = reinterpret_cast<uint64_t *>(base + o_P);
   char *cs = base + o_cs;
   const uint64_t chunks = cdiv(n, C);
+  // pageable spans: staged through the pinned slots (see the merge above)
+  const bool stage_in = is_pageable(keys) || (VALS && is_pageable(vals));
+  const bool stage_out = is_pageable(out_keys) || (VALS && is_pageable(out_vals));
+  const uint64_t pin_v = up(C * ks), pin_slot = (pin_v + (VALS ? up(C * 4) : 0) + 4095) & ~4095ull;
+  if (stage_in || stage_out)
+    if (int rc = hp.reserve_pinned(pin_slot * kSlots))
+      return rc;
+  std::vector<std::tuple<void *, const void *, size_t>> jobs;
   for (uint64_t c = 0; c < chunks; ++c) {
     const int sl = static_cast<int>(c % kSlots);
     const uint64_t off = c * C, len = std::min<uint64_t>(C, n - off);
-    MP_CUDA(cudaMemcpyAsync(d + off, keys + off, len * ks, cudaMemcpyHostToDevice, hp.h2d));
+    const void *kin = keys + off, *vin = VALS ? vals + off : nullptr;
+    if (stage_in) {
+      char *pin = static_cast<char *>(hp.pin) + sl * pin_slot;
+      if (c >= kSlots)  // the slot's previous H2D copy has read it
+        MP_CUDA(cudaEventSynchronize(hp.ev_h2d[sl]));
+      jobs.clear();
+      jobs.emplace_back(pin, kin, len * ks);
+      if (VALS)
+        jobs.emplace_back(pin + pin_v, vin, len * 4);
+      CopyPool::get().copy(jobs);
+      kin = pin;
+      vin = pin + pin_v;
+    }
+    MP_CUDA(cudaMemcpyAsync(d + off, kin, len * ks, cudaMemcpyHostToDevice, hp.h2d));
     if (VALS)
-      MP_CUDA(cudaMemcpyAsync(dv + off, vals + off, len * 4, cudaMemcpyHostToDevice, hp.h2d));
+      MP_CUDA(cudaMemcpyAsync(dv + off, vin, len * 4, cudaMemcpyHostToDevice, hp.h2d));
     MP_CUDA(cudaEventRecord(hp.ev_h2d[sl], hp.h2d));
     MP_CUDA(cudaStreamWaitEvent(hp.cmp, hp.ev_h2d[sl], 0));
     if (int rc = sort_impl<KT, VALS>(d + off, VALS ? dv + off : nullptr, d + off,
@@ -1836,10 +2069,46 @@ int sort_host_pipelined(const void *keys_, const uint32_t *vals, uint64_t n,
   uint32_t *resv = nullptr;
   if (int rc = sort_rounds_from<KT, VALS>(d, dv, aux, auxv, n, C, NV, P, hp.cmp, &res, &resv))
     return rc;
-  MP_CUDA(cudaMemcpyAsync(out_keys, res, n * ks, cudaMemcpyDeviceToHost, hp.cmp));
-  if (VALS)
-    MP_CUDA(cudaMemcpyAsync(out_vals, resv, n * 4, cudaMemcpyDeviceToHost, hp.cmp));
-  MP_CUDA(cudaStreamSynchronize(hp.cmp));
+  if (!stage_out) {
+    MP_CUDA(cudaMemcpyAsync(out_keys, res, n * ks, cudaMemcpyDeviceToHost, hp.cmp));
+    if (VALS)
+      MP_CUDA(cudaMemcpyAsync(out_vals, resv, n * 4, cudaMemcpyDeviceToHost, hp.cmp));
+    MP_CUDA(cudaStreamSynchronize(hp.cmp));
+    *done = true;
+    return MP_OK;
+  }
+  // pageable output: chunk j lands in pinned slot j % kSlots (D2H stream)
+  // and is copied out by the pool while chunk j + 1 is in flight
+  MP_CUDA(cudaEventRecord(hp.ev_cmp[0], hp.cmp));
+  MP_CUDA(cudaStreamWaitEvent(hp.d2h, hp.ev_cmp[0], 0));
+  auto drain = [&](uint64_t j) -> int {
+    const int sj = static_cast<int>(j % kSlots);
+    const char *pin = static_cast<const char *>(hp.pin) + sj * pin_slot;
+    const uint64_t off = j * C, len = std::min<uint64_t>(C, n - off);
+    MP_CUDA(cudaEventSynchronize(hp.ev_d2h[sj]));
+    jobs.clear();
+    jobs.emplace_back(static_cast<T *>(out_keys) + off, pin, len * ks);
+    if (VALS)
+      jobs.emplace_back(out_vals + off, pin + pin_v, len * 4);
+    CopyPool::get().copy(jobs);
+    return MP_OK;
+  };
+  for (uint64_t j = 0; j < chunks; ++j) {
+    const int sj = static_cast<int>(j % kSlots);
+    char *pin = static_cast<char *>(hp.pin) + sj * pin_slot;
+    const uint64_t off = j * C, len = std::min<uint64_t>(C, n - off);
+    MP_CUDA(cudaMemcpyAsync(pin, res + off, len * ks, cudaMemcpyDeviceToHost, hp.d2h));
+    if (VALS)
+      MP_CUDA(cudaMemcpyAsync(pin + pin_v, resv + off, len * 4, cudaMemcpyDeviceToHost, hp.d2h));
+    MP_CUDA(cudaEventRecord(hp.ev_d2h[sj], hp.d2h));
+    if (j >= kDrainLag)
+      if (int rc = drain(j - kDrainLag))
+        return rc;
+  }
+  for (uint64_t j = chunks > kDrainLag ? chunks - kDrainLag : 0; j < chunks; ++j)
+    if (int rc = drain(j))
+      return rc;
+  MP_CUDA(cudaStreamSynchronize(hp.d2h));
   *done = true;
   return MP_OK;
 }
@@ -1904,6 +2173,23 @@ int mp_sort_host(int kt, const void *keys, const uint32_t *vals, uint64_t n,
   return MP_OK;
 }
 
+void *mp_host_alloc(uint64_t bytes) {
+  g_err.clear();
+  void *p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    cuda_fail(cudaGetLastError(), "cudaHostAlloc");
+    return nullptr;
+  }
+  return p;
+}
+
+int mp_host_free(void *p) {
+  g_err.clear();
+  if (p)
+    MP_CUDA(cudaFreeHost(p));
+  return MP_OK;
+}
+
 int mp_release(int device) {
   g_err.clear();
   int count = 0;
@@ -1921,6 +2207,11 @@ int mp_release(int device) {
       MP_CUDA(cudaFree(P.buf));
       P.buf = nullptr;
       P.buf_bytes = 0;
+    }
+    if (P.pin) {
+      MP_CUDA(cudaFreeHost(P.pin));
+      P.pin = nullptr;
+      P.pin_bytes = 0;
     }
   }
   if (g_pools[device])

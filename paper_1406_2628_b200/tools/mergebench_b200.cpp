@@ -4,10 +4,10 @@
 //   mergebench_b200 gen    --dist D --na N --nb N [--seed S] --out-a F --out-b F [--format bin|text]
 //   mergebench_b200 merge  --a F --b F [--variant regular|segmented] [--threads 1,2,..]
 //                          [--cache-elems C,..] [--reps R] [--sink memory|register]
-//                          [--format json|csv] [--out F] [--residency device|host] [--device N]
+//                          [--format json|csv] [--out F] [--residency device|host] [--host-memory pinned|pageable] [--device N]
 //   mergebench_b200 sort   --in F [--variant plain|cache_efficient] [--threads ..]
 //                          [--cache-elems C] [--reps R] [--format json|csv] [--out F]
-//                          [--residency device|host] [--device N]
+//                          [--residency device|host] [--host-memory pinned|pageable] [--device N]
 //   mergebench_b200 report --in F [--format json|csv] [--out F]
 //
 // Same subcommands, flags, report rows {op, variant, n, p, cache_elems, reps,
@@ -680,6 +680,11 @@ int run_merge(const Args &a) {
   member("format", format, {"json", "csv"});
   const std::string residency = opt(a, "residency", "device");
   member("residency", residency, {"device", "host"});
+  // host residency: page-lock the tool's vectors before timing (pinned) or
+  // leave them pageable -- what a plain std::vector caller passes; the
+  // library then stages the chunks through pinned slots
+  const std::string host_memory = opt(a, "host-memory", "pinned");
+  member("host-memory", host_memory, {"pinned", "pageable"});
   const std::size_t reps = reps_of(a, 5);
   auto threads = a.kv.count("threads") ? to_list("threads", a.kv.at("threads"))
                                        : thread_sweep();
@@ -719,7 +724,7 @@ int run_merge(const Args &a) {
   std::vector<Row> rows;
   std::vector<std::int64_t> out(n);
   std::unique_ptr<PinScope> pa, pb, po;
-  if (residency == "host") {
+  if (residency == "host" && host_memory == "pinned") {
     pa = std::make_unique<PinScope>(const_cast<std::int64_t *>(A.data()), A.size() * 8);
     pb = std::make_unique<PinScope>(const_cast<std::int64_t *>(B.data()), B.size() * 8);
     po = std::make_unique<PinScope>(out.data(), out.size() * 8);
@@ -808,6 +813,7 @@ int run_merge(const Args &a) {
   meta.set("backend", Json::string("b200"));
   meta.set("device", Json::string(device_name(dev)));
   meta.set("residency", Json::string(residency));
+  meta.set("host_memory", Json::string(residency == "host" ? host_memory : "n/a"));
   Json report = Json::object();
   report.set("meta", meta);
   Json arr = Json::array();
@@ -827,6 +833,11 @@ int run_sort(const Args &a) {
   member("format", format, {"json", "csv"});
   const std::string residency = opt(a, "residency", "device");
   member("residency", residency, {"device", "host"});
+  // host residency: page-lock the tool's vectors before timing (pinned) or
+  // leave them pageable -- what a plain std::vector caller passes; the
+  // library then stages the chunks through pinned slots
+  const std::string host_memory = opt(a, "host-memory", "pinned");
+  member("host-memory", host_memory, {"pinned", "pageable"});
   const std::size_t reps = reps_of(a, 3);
   const std::size_t cache = static_cast<std::size_t>(
       to_u64("cache-elems", opt(a, "cache-elems", std::to_string(3 * 4096))));
@@ -852,7 +863,7 @@ int run_sort(const Args &a) {
   }
   std::vector<Row> rows;
   std::unique_ptr<PinScope> pin_in;
-  if (residency == "host")
+  if (residency == "host" && host_memory == "pinned")
     pin_in = std::make_unique<PinScope>(const_cast<std::int64_t *>(data.data()), n * 8);
   for (std::size_t p : threads) {
     if (p == 0)
@@ -909,6 +920,7 @@ int run_sort(const Args &a) {
   meta.set("backend", Json::string("b200"));
   meta.set("device", Json::string(device_name(dev)));
   meta.set("residency", Json::string(residency));
+  meta.set("host_memory", Json::string(residency == "host" ? host_memory : "n/a"));
   Json report = Json::object();
   report.set("meta", meta);
   Json arr = Json::array();
@@ -943,10 +955,10 @@ void usage(std::ostream &out) {
          "         [--seed S] --out-a F --out-b F [--format bin|text]\n"
          "  merge  --a F --b F [--variant regular|segmented] [--threads P,..]\n"
          "         [--cache-elems C,..] [--reps R>=3] [--sink memory|register]\n"
-         "         [--format json|csv] [--out F] [--residency device|host] [--device N]\n"
+         "         [--format json|csv] [--out F] [--residency device|host] [--host-memory pinned|pageable] [--device N]\n"
          "  sort   --in F [--variant plain|cache_efficient] [--threads P,..]\n"
          "         [--cache-elems C] [--reps R>=3] [--format json|csv] [--out F]\n"
-         "         [--residency device|host] [--device N]\n"
+         "         [--residency device|host] [--host-memory pinned|pageable] [--device N]\n"
          "  report --in F [--format json|csv] [--out F]\n";
 }
 
@@ -969,11 +981,11 @@ int main(int argc, char **argv) {
     if (cmd == "merge")
       return run_merge(parse_args(argc, argv, 2,
                                   {"a", "b", "variant", "threads", "cache-elems", "reps",
-                                   "sink", "format", "out", "residency", "device"}));
+                                   "sink", "format", "out", "residency", "host-memory", "device"}));
     if (cmd == "sort")
       return run_sort(parse_args(argc, argv, 2,
                                  {"in", "variant", "threads", "cache-elems", "reps",
-                                  "format", "out", "residency", "device"}));
+                                  "format", "out", "residency", "host-memory", "device"}));
     if (cmd == "report")
       return run_report(parse_args(argc, argv, 2, {"in", "format", "out"}));
     if (cmd == "cachesim")

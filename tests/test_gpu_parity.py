@@ -944,3 +944,44 @@ def test_split_search_paths_vs_oracle(cuda, fuse_tiles, k4_warp):
                        env=dict(os.environ, MP_MERGE_FUSE_TILES=fuse_tiles,
                                 MP_K4_WARP_TILES=k4_warp))
     assert r.returncode == 0 and " passed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("S", ["i32", "u64"])
+def test_pageable_host_spans_staged(cuda, port, S):
+    """Host calls on pageable memory (numpy arrays, i.e. what a std::vector
+    caller passes) go through the pinned staging slots and the copy pool:
+    several chunks (1 MiB chunk override in a subprocess is not needed --
+    the sizes span many 64 MiB chunks for u64 with values), unaligned
+    sub-views, values; results equal the oracle and the pinned call."""
+    import torch
+    from paper_1406_2628_b200 import _native as N
+    rng = np.random.default_rng(77)
+    kt = key_type(S)
+    dt = np.int32 if S == "i32" else np.uint64
+    na, nb = (40_000_001, 27_000_013) if S == "i32" else (12_000_007, 9_000_001)
+    a = np.sort(rng.integers(0, 1 << 20, na + 3).astype(dt))[3:]  # unaligned view
+    b = np.sort(rng.integers(0, 1 << 20, nb).astype(dt))
+    av = np.arange(na, dtype=np.uint32)
+    bv = np.arange(nb, dtype=np.uint32) | np.uint32(1 << 31)
+    out = np.empty(na + nb + 1, dtype=dt)[1:]
+    outv = np.empty(na + nb, dtype=np.uint32)
+    N.check(N.lib.mp_merge_host(kt, a.ctypes.data, av.ctypes.data, na, b.ctypes.data,
+                                bv.ctypes.data, nb, out.ctypes.data, outv.ctypes.data, 0))
+    want, wantv, _, _ = port.merge(S, a, b, av=av, bv=bv)
+    assert np.array_equal(out, want) and np.array_equal(outv, wantv)
+    # the pinned path gives the same bytes
+    pa = torch.from_numpy(a.copy()).pin_memory()
+    pb = torch.from_numpy(b.copy()).pin_memory()
+    po = torch.empty(na + nb, dtype=pa.dtype).pin_memory()
+    N.check(N.lib.mp_merge_host(kt, pa.data_ptr(), None, na, pb.data_ptr(), None, nb,
+                                po.data_ptr(), None, 0))
+    assert np.array_equal(po.numpy(), want)
+    # the sort from pageable memory (chunked H2D staging + chunked D2H drain)
+    x = rng.integers(0, 1 << 20, 3 * (1 << 24) + 5).astype(dt)
+    v = np.arange(len(x), dtype=np.uint32)
+    xo = np.empty_like(x)
+    vo = np.empty_like(v)
+    N.check(N.lib.mp_sort_host(kt, x.ctypes.data, v.ctypes.data, len(x), xo.ctypes.data,
+                               vo.ctypes.data, 0))
+    perm = np.argsort(x, kind="stable")
+    assert np.array_equal(xo, x[perm]) and np.array_equal(vo, v[perm].astype(np.uint32))
