@@ -56,13 +56,13 @@ CONFIGS = {
     "3b": dict(kind="merge", key="u64", gen=(4, 3), na=1 << 29, nb=1 << 25, bytes_per=24, vals=True,
                desc="config3b: stable merge u64 key + u32 value, |A|=2^29 |B|=2^25, B below A"),
     "4": dict(kind="sort", key="u32", gen=(0, None), n=1 << 30, bytes_per=160,
-              desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 8192-key block sort + 17 merge rounds "
-                   "(run as 8 fused round pairs + 1 round)"),
+              desc="config4: stable merge sort of 2^30 u32 keys, seed 4: 16384-key block sort + 16 merge "
+                   "rounds (run as 8 fused round pairs)"),
     "5": dict(kind="merge", key="f32", gen=(5, 6), na=1 << 31, nb=1 << 31, bytes_per=8, sharded=True,
               desc="config5: stable merge f32 |A|=|B|=2^31, A~Normal(0,1), B~Exp(1), IEEE "
                    "totalOrder (one GPU: the whole merge; --gpus 8: sharded)"),
 }
-BARE_RUN = 8192  # mp_sort's block-sort run for bare 32-bit keys (K3w: 512 threads x 16)
+BARE_RUN = 16384  # mp_sort's block-sort run for bare 32-bit keys (K3w: 512 threads x 32)
 
 
 def config_dict(cfg, ws):
@@ -298,8 +298,8 @@ def run_ours(args, cfg, ws, rank, local, dist_on):
     else:
         alg_bytes = n * 8 * (1 + sort_rounds(n))
         kname = ("mp_sort: block_sort_warp + 8 x fused round pair (quad_partition + quad_refine + "
-                 "quad_tile) + 1 x (round_partition + merge_tiles); algorithmic bytes count every "
-                 "round as a full pass (SURVEY 8d), the fused pairs move half of them")
+                 "quad_tile); algorithmic bytes count every round as a full pass (SURVEY 8d), the "
+                 "fused pairs move half of them")
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     traffic, traffic_src = None, "no ncu capture for this config"
     tpath = ROOT / "profiles" / f"traffic_config{args.config}.json"

@@ -191,12 +191,19 @@ template <class KT> struct SortMergeCfg {
 constexpr int kBlockNT = 128;
 constexpr int kBlockVT = 16;
 constexpr uint64_t kRun = kBlockNT * kBlockVT;  // 2048-key block-sort runs
-// bare 32-bit keys: K3w (mp_bsort.cuh), 16 keys per thread
+// bare 32-bit keys: K3w (mp_bsort.cuh)
 #ifndef MP_WARP_NT
-#define MP_WARP_NT 512  // 8192-key runs: one round fewer (17 at 2^30) for
-#endif                  // one more smem pass; B200 2^30 u32 31.52 -> 31.36 ms
+#define MP_WARP_NT 512
+#endif
 constexpr int kWarpNT = MP_WARP_NT;
-constexpr uint64_t kWarpRun = kWarpNT * 16;
+// K3w shape: 512 threads x 32 keys = 16384-key runs, so a 2^30-key sort is
+// 16 rounds = 8 fused round pairs with no plain round left over.  B200 A/B
+// (tools/ab_k3w_shape.sh, whole 2^30 sort / K3w alone, 1965 MHz): 512 x 16
+// (8192-key runs, 4 smem passes) 27.27 / 7.59 ms; 256 x 32 (8192-key runs,
+// 3 smem passes) 26.68 / 7.00 ms; 512 x 32 26.53 / 8.05 ms.
+constexpr int kWarpVT = 32;
+uint64_t warp_run() { return uint64_t(kWarpNT) * kWarpVT; }
+
 constexpr uint32_t kBigTile4 = 8192;  // round tile after K3w (sort_round_tile)
 constexpr int kBigTileNT = 384;       // 384 x 23 >= 8192
 // K5e (fused two-round pass) thread shape at the 8192-output tile:
@@ -436,7 +443,7 @@ bool block_sort_generic() {
 // Run length the block sort leaves and the round tile (mp_sort's schedule).
 template <class KT, bool VALS> uint64_t sort_run0() {
   constexpr bool bare4 = !VALS && sizeof(typename KT::T) == 4 && KT::kind != kElement;
-  return bare4 && !block_sort_generic() ? kWarpRun : kRun;
+  return bare4 && !block_sort_generic() ? warp_run() : kRun;
 }
 // Fused two-round passes (mp_quad.cuh) for bare 32-bit sorts whose rounds
 // are too large for the in-kernel split search: default on, MP_SORT_QUAD=0
@@ -550,8 +557,8 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   uint64_t *P = reinterpret_cast<uint64_t *>(ws + L.part_off);
 
   constexpr bool kBare4 = !VALS && sizeof(T) == 4 && KT::kind != kElement;
-  const bool use_warp = kBare4 && !block_sort_generic();  // K3w, kWarpRun-key runs
-  const uint64_t run0 = use_warp ? kWarpRun : kRun;
+  const bool use_warp = kBare4 && !block_sort_generic();  // K3w runs
+  const uint64_t run0 = use_warp ? warp_run() : kRun;
   int rounds = 0;
   for (uint64_t w = run0; w < n; w *= 2)
     ++rounds;
@@ -577,16 +584,17 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
   if (use_warp) {
     if constexpr (kBare4) {
       const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
-      const uint64_t whole = al ? n / kWarpRun : 0, blocks = cdiv(n, kWarpRun);
-      constexpr uint32_t smem = warp_sort_smem_bytes<kWarpNT>();
+      constexpr uint64_t run = uint64_t(kWarpNT) * kWarpVT;
+      const uint64_t whole = al ? n / run : 0, blocks = cdiv(n, run);
+      constexpr uint32_t smem = warp_sort_smem_bytes<kWarpNT, kWarpVT>();
       if (whole) {
-        auto kern = block_sort_warp_kernel<KT, kWarpNT, true>;
+        auto kern = block_sort_warp_kernel<KT, kWarpNT, true, kWarpVT>;
         MP_CUDA(set_smem(kern, smem));
         kern<<<static_cast<unsigned>(whole), kWarpNT, smem, s>>>(in, src, n, 0);
         MP_LAUNCHED("block_sort_warp_kernel");
       }
       if (blocks > whole) {
-        auto kern = block_sort_warp_kernel<KT, kWarpNT, false>;
+        auto kern = block_sort_warp_kernel<KT, kWarpNT, false, kWarpVT>;
         MP_CUDA(set_smem(kern, smem));
         kern<<<static_cast<unsigned>(blocks - whole), kWarpNT, smem, s>>>(in, src, n, whole);
         MP_LAUNCHED("block_sort_warp_kernel(tail)");

@@ -465,11 +465,11 @@ def make_sort_plan(variant: SortVariant, n: int, cache_elems: int) -> SortPlan:
 
 
 GPU_SORT_RUN = 2048       # stable K3 block sort (values, 64-bit keys, element)
-GPU_SORT_RUN_BARE = 8192  # K3w block sort (bare u32 / i32 / f32 keys)
+GPU_SORT_RUN_BARE = 16384  # K3w block sort (bare u32 / i32 / f32 keys)
 
 
 def gpu_sort_plan(n: int, bare32: bool = False) -> SortPlan:
-    """The B200 schedule: block-sorted runs (8192 keys for bare 32-bit keys,
+    """The B200 schedule: block-sorted runs (16384 keys for bare 32-bit keys,
     2048 otherwise), then ceil(log2(n/run)) Merge Path rounds (large bare
     32-bit sorts run them as fused pairs: one HBM pass per two rounds)."""
     run = GPU_SORT_RUN_BARE if bare32 else GPU_SORT_RUN

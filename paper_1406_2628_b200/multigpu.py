@@ -669,7 +669,7 @@ def _overlap(lo, hi, s0, s1):
     return max(0, min(hi, s1) - max(lo, s0))
 
 
-def sort_traffic(comm, trace, lens, run0=8192):
+def sort_traffic(comm, trace, lens, run0=16384):
     """Collective.  Per-rank, per-phase element counts of one P2PSorter.run
     (from a traced run): phase 0 = the local sort (its algorithmic HBM
     passes: block sort + ceil(log2(n/run0)) rounds, each reading and writing

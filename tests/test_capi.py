@@ -116,8 +116,8 @@ def test_sort_plan_kats(kats):
                 assert getattr(plan, key) == c[key], c["src"]
     gp = mp.gpu_sort_plan(1 << 30)
     assert gp.block_size == 2048 and gp.tree_levels == 19
-    gp = mp.gpu_sort_plan(1 << 30, bare32=True)  # config 4: 8192-key runs, 17 rounds
-    assert gp.block_size == 8192 and gp.tree_levels == 17
+    gp = mp.gpu_sort_plan(1 << 30, bare32=True)  # config 4: 16384-key runs, 16 rounds
+    assert gp.block_size == 16384 and gp.tree_levels == 16
 
 
 def test_custom_comparator_rejected():

@@ -606,7 +606,7 @@ print("FUSED OK")
 @pytest.mark.parametrize("engine,quad", [("warp", "0"), ("warp", "1"), ("merge", "0"),
                                         ("merge", "1")])
 def test_fused_round_sorts_vs_oracle(cuda, S, engine, quad):
-    """Bare 32-bit sorts through each block sort -- K3w (default, 8192-key
+    """Bare 32-bit sorts through each block sort -- K3w (default, 16384-key
     runs, warp bitonic levels + Merge Path passes) and the stable K3
     (MP_BLOCK_SORT=merge, 2048-key runs) -- then plain rounds or fused
     two-round passes (MP_SORT_QUAD=1, mp_quad.cuh) at every size.  The
@@ -623,7 +623,7 @@ def test_fused_round_sorts_vs_oracle(cuda, S, engine, quad):
 
 
 def _fused_round_cases(cuda, S):
-    """Sizes straddle run and group boundaries (runs of 8192 and 2048,
+    """Sizes straddle run and group boundaries (runs of 16384 and 2048,
     groups of 4 runs) so the short last group has 1, 2 or 3 runs; inputs
     include heavy duplicates, all-equal, descending and (f32) signed zeros /
     NaNs."""
@@ -632,7 +632,7 @@ def _fused_round_cases(cuda, S):
     port = bindings.port()
     rng = np.random.default_rng(29)
     sizes = (511, 512, 513, 4095, 4096, 4097, 8191, 8193, 200_003, 1_000_000)
-    for R in (8192, 2048):
+    for R in (16384, 2048):
         sizes += (4 * R - 1, 4 * R, 4 * R + 1, 5 * R + 7, 6 * R, 7 * R + 3, 16 * R + 1,
                   16 * R + 9 * R, 64 * R - 5)
     for n in sizes:
