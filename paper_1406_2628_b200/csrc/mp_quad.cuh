@@ -395,11 +395,25 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
   };
   Hdr *hdr = reinterpret_cast<Hdr *>(smem + 16);
   constexpr uint32_t kWin0 = 64;
-  if (tid < 32) {
+  // The windows travel as whole 16-byte granules: one bulk copy per window
+  // covers its unaligned head and tail too (the extra bytes land in the gap
+  // before the window and in its sentinel area, which is written after the
+  // copy), so warp 0's setup is one dependent load (the split points) and
+  // the copy issue -- no edge loads.  Only where a granule would leave the
+  // array (its first / last window) are those < 16 bytes read by plain
+  // loads.  The other warps wait on the mbarrier for the copies and the
+  // header, then one barrier orders the sentinel stores.
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uintptr_t arr_lo = reinterpret_cast<uintptr_t>(src);
+  const uintptr_t arr_hi = reinterpret_cast<uintptr_t>(src + n);
+  if (tid == 0) {
     const uint64_t t = blockIdx.x;
     const uint64_t pos = t * T;
-    // 4w is a power of two after K3w's runs (lg4w < 64); K3b's 4352-key
-    // runs are not (lg4w = ~0u): divide
+    // 4w is a power of two after K3w's runs (lg4w < 64); otherwise divide
     const uint64_t g = lg4w < 64 ? (pos >> lg4w) : pos / (4 * w);
     const QuadGroup q = quad_group(g, n, w);
     const QuadPt p0 = Q[t];
@@ -412,53 +426,40 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
       for (int r = 0; r < 4; ++r)
         p1.i[r] = q.l[r];
     }
-    int cnt[4];
-    const char *gW[4];
+    uint32_t at = kWin0, tx = 0;
+    uintptr_t wa[4], wb[4];
     uint32_t oW[4];
-    uint32_t at = kWin0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      cnt[r] = static_cast<int>(p1.i[r] - p0.i[r]);
-      gW[r] = reinterpret_cast<const char *>(src + q.S + r * w + p0.i[r]);
-      oW[r] = mirror_off(at, gW[r]);
-      at = oW[r] + cnt[r] * KS + quad_gap_bytes<KT, VT>();
+      const int c = static_cast<int>(p1.i[r] - p0.i[r]);
+      const uintptr_t s0 = reinterpret_cast<uintptr_t>(src + q.S + r * w + p0.i[r]);
+      const uintptr_t e0 = s0 + c * KS;
+      oW[r] = mirror_off(at, reinterpret_cast<const void *>(s0));
+      at = oW[r] + c * KS + quad_gap_bytes<KT, VT>();
+      uintptr_t a = s0 & ~uintptr_t(15), b = (e0 + 15) & ~uintptr_t(15);
+      if (a < arr_lo)
+        a = (s0 + 15) & ~uintptr_t(15);
+      if (b > arr_hi)
+        b = e0 & ~uintptr_t(15);
+      if (!c || b <= a)
+        a = b = 0;
+      wa[r] = a;
+      wb[r] = b;
+      tx += static_cast<uint32_t>(b - a);
+      hdr->oW[r] = oW[r];
+      hdr->cnt[r] = c;
     }
-    const int l = tid;
-    if (l == 0) {
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        hdr->oW[r] = oW[r];
-        hdr->cnt[r] = cnt[r];
-      }
-      hdr->o0 = pos;
-      mbar_init(bar, 1);
-      fence_mbar_init();
-      uint32_t lo[4], ib[4], tx = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        ib[r] = interior_bytes(gW[r], cnt[r] * KS, &lo[r]);
-        tx += ib[r];
-      }
-      mbar_arrive_expect_tx(bar, tx);
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (ib[r])
-          bulk_g2s(smem + oW[r] + lo[r], gW[r] + lo[r], ib[r], bar);
-    }
+    hdr->o0 = pos;
+    mbar_arrive_expect_tx(bar, tx);
 #pragma unroll
     for (int r = 0; r < 4; ++r)
-      if ((l >> 3) == r)
-        stage_edges<KS>(smem, oW[r], gW[r], cnt[r] * KS, l & 7);
-    // sentinels behind the windows (outside every bulk-copy destination)
-    if (l < VT) {
-      *reinterpret_cast<T_ *>(smem + oW[0] + (cnt[0] + l) * KS) = KT::max_key();
-      *reinterpret_cast<T_ *>(smem + oW[2] + (cnt[2] + l) * KS) = KT::max_key();
-    } else if (l == VT) {
-      *reinterpret_cast<T_ *>(smem + oW[1] + cnt[1] * KS) = KT::max_key();
-      *reinterpret_cast<T_ *>(smem + oW[3] + cnt[3] * KS) = KT::max_key();
-    }
+      if (wb[r] > wa[r]) {
+        const uintptr_t s0 = reinterpret_cast<uintptr_t>(src + q.S + r * w + p0.i[r]);
+        bulk_g2s(smem + oW[r] - static_cast<uint32_t>(s0 - wa[r]),
+                 reinterpret_cast<const void *>(wa[r]), static_cast<uint32_t>(wb[r] - wa[r]), bar);
+      }
   }
-  __syncthreads();
+  mbar_wait(bar, 0);
   uint32_t oW[4];
   int cnt[4];
 #pragma unroll
@@ -468,7 +469,47 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
   }
   const uint64_t o0 = hdr->o0;
   const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
-  mbar_wait(bar, 0);
+  {
+    const int w_ = tid >> 5, l = tid & 31;
+    if (w_ == 0) {  // sentinels behind the windows (after the copies landed)
+      if (l < VT) {
+        *reinterpret_cast<T_ *>(smem + oW[0] + (cnt[0] + l) * KS) = KT::max_key();
+        *reinterpret_cast<T_ *>(smem + oW[2] + (cnt[2] + l) * KS) = KT::max_key();
+      } else if (l == VT) {
+        *reinterpret_cast<T_ *>(smem + oW[1] + cnt[1] * KS) = KT::max_key();
+        *reinterpret_cast<T_ *>(smem + oW[3] + cnt[3] * KS) = KT::max_key();
+      }
+    } else if (w_ == 1) {  // window edges a granule would have read outside the array
+      const int r = l >> 3, e = l & 7;
+      const uint32_t oWr = r == 0 ? oW[0] : r == 1 ? oW[1] : r == 2 ? oW[2] : oW[3];
+      const int cr = r == 0 ? cnt[0] : r == 1 ? cnt[1] : r == 2 ? cnt[2] : cnt[3];
+      const uint64_t pos = o0;
+      const uint64_t g = lg4w < 64 ? (pos >> lg4w) : pos / (4 * w);
+      // window r's first element: the tile's split point, recomputed from Q
+      const QuadPt p0 = Q[blockIdx.x];
+      const uintptr_t s0 = reinterpret_cast<uintptr_t>(src + g * 4 * w + r * w + p0.i[r]);
+      const uintptr_t e0 = s0 + cr * KS;
+      if (cr && (((s0 & ~uintptr_t(15)) < arr_lo) || (((e0 + 15) & ~uintptr_t(15)) > arr_hi))) {
+        uintptr_t a = s0 & ~uintptr_t(15), b = (e0 + 15) & ~uintptr_t(15);
+        if (a < arr_lo)
+          a = (s0 + 15) & ~uintptr_t(15);
+        if (b > arr_hi)
+          b = e0 & ~uintptr_t(15);
+        if (b <= a)
+          a = b = e0;  // nothing came by bulk copy: plain loads for all
+        const uint32_t nh = static_cast<uint32_t>((a > s0 ? a - s0 : 0) / KS);
+        const uint32_t nt = static_cast<uint32_t>((e0 > b ? e0 - b : 0) / KS);
+        // head [s0, a) and tail [b, e0): at most 3 + 3 elements (or the
+        // whole window of <= 7 elements when no granule fits)
+        for (uint32_t k = e; k < nh + nt; k += 8) {
+          const uintptr_t gaddr = k < nh ? s0 + k * KS : b + (k - nh) * KS;
+          *reinterpret_cast<T_ *>(smem + oWr + (gaddr - s0)) =
+              *reinterpret_cast<const T_ *>(gaddr);
+        }
+      }
+    }
+  }
+  __syncthreads();
 
   // ---- phase 1: dynamic split of the threads between X and Y ----
   T_ keys[VT];
