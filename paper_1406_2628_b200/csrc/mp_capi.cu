@@ -200,8 +200,13 @@ constexpr int kWarpNT = MP_WARP_NT;
 // 16 rounds = 8 fused round pairs with no plain round left over.  B200 A/B
 // (tools/ab_k3w_shape.sh, whole 2^30 sort / K3w alone, 1965 MHz): 512 x 16
 // (8192-key runs, 4 smem passes) 27.27 / 7.59 ms; 256 x 32 (8192-key runs,
-// 3 smem passes) 26.68 / 7.00 ms; 512 x 32 26.53 / 8.05 ms.
-constexpr int kWarpVT = 32;
+// 3 smem passes) 26.68 / 7.00 ms; 512 x 32 26.53 / 8.05 ms; 256 x 64
+// (16384-key runs, 3 smem passes, 80 registers, tools/ab_k3w_v64.sh) 26.27 /
+// 8.04 ms with K5e's granule copies vs 26.27-26.34 for 512 x 32: no gain.
+#ifndef MP_K3W_VT
+#define MP_K3W_VT 32
+#endif
+constexpr int kWarpVT = MP_K3W_VT;
 uint64_t warp_run() { return uint64_t(kWarpNT) * kWarpVT; }
 
 constexpr uint32_t kBigTile4 = 8192;  // round tile after K3w (sort_round_tile)
