@@ -616,3 +616,71 @@ __global__ void __launch_bounds__(NTC + 32, NBUF == 1 ? 2 : 1)
   }
 }
 
+
+
+// ===== K5e with two merge chains per thread (MP_K5E_CHAINS=2, round 2):
+// each thread's VT outputs as two halves from two splits (the second by a
+// short search bounded by the first), stepped alternately for ILP.  B200
+// (tools/ab_k5e_chains.sh): K5e 2.09 -> 2.26 ms per pass, sort 26.3 ->
+// 27.6-27.7 ms (48 registers either way; the extra search costs more than
+// the shorter chains save).  Not kept.
+// Two independent merge chains per thread (bare keys on sentinels, as
+// serial_merge SENT): outputs [0, H) from split (i0, j0) and [H, VT) from
+// split (i1, j1), stepped alternately so each dependent LDS -> compare ->
+// select chain has the other one's instructions to hide behind.
+template <class KT, int VT, int H>
+__device__ __forceinline__ void serial_merge2(const char *smem, uint32_t oA, uint32_t oB,
+                                              int i0, int j0, int i1, int j1,
+                                              typename KT::T (&keys)[VT]) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  uint32_t pa0 = oA + i0 * KS, pb0 = oB + j0 * KS;
+  uint32_t pa1 = oA + i1 * KS, pb1 = oB + j1 * KS;
+  T ka0 = lds<T>(smem, pa0), kb0 = lds<T>(smem, pb0);
+  T ka1 = lds<T>(smem, pa1), kb1 = lds<T>(smem, pb1);
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    {
+      const bool tb = take_b<KT>(kb0, ka0);
+      keys[k] = tb ? kb0 : ka0;
+      pa0 += tb ? 0u : KS;
+      pb0 += tb ? KS : 0u;
+      const T nxt = lds<T>(smem, tb ? pb0 : pa0);
+      kb0 = tb ? nxt : kb0;
+      ka0 = tb ? ka0 : nxt;
+    }
+    if (H + k < VT) {
+      const bool tb = take_b<KT>(kb1, ka1);
+      keys[H + k] = tb ? kb1 : ka1;
+      pa1 += tb ? 0u : KS;
+      pb1 += tb ? KS : 0u;
+      const T nxt = lds<T>(smem, tb ? pb1 : pa1);
+      kb1 = tb ? nxt : kb1;
+      ka1 = tb ? ka1 : nxt;
+    }
+  }
+}
+
+// Split on diagonal d knowing the split on diagonal d0 < d is a0: it lies
+// in [a0, a0 + (d - d0)] (and the usual range) -- a short search.
+template <class KT>
+__device__ __forceinline__ int split_after(const char *smem, uint32_t oA, int na, uint32_t oB,
+                                           int nb, int d, int d0, int a0) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  int lo = max(d > nb ? d - nb : 0, a0);
+  int hi = min(d < na ? d : na, a0 + (d - d0));
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (take_b<KT>(lds<T>(smem, oB + (d - 1 - mid) * KS), lds<T>(smem, oA + mid * KS)))
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+#ifndef MP_K5E_CHAINS
+#define MP_K5E_CHAINS 2
+#endif
+
