@@ -135,6 +135,56 @@ struct DeviceScope {  // restores the caller's current device
 
 uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+// Allocation holding p: cuMemGetAddressRange through the runtime's driver
+// entry point (no link-time dependency on libcuda).  false if unknown.
+bool alloc_range(const void *p, uintptr_t *base, size_t *size) {
+  using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+  static GetRange get_range = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      fn = nullptr;
+    }
+    return reinterpret_cast<GetRange>(fn);
+  }();
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (!get_range || get_range(&b, &sz, reinterpret_cast<unsigned long long>(p)) != 0)
+    return false;
+  *base = static_cast<uintptr_t>(b);
+  *size = sz;
+  return true;
+}
+
+// Allocations of other processes mapped into this one (mp_ipc_import),
+// per importing device, reference counted (mp_ipc_close).
+struct IpcMapping {
+  int dev;
+  std::string handle;
+  void *base;
+  size_t size;
+  size_t refs;
+};
+std::mutex g_ipc_mu;
+std::vector<IpcMapping> g_ipc;
+
+// Is p inside memory mapped from another process?  Such memory may live on
+// another GPU whatever the pointer attributes report, so the piece merge
+// reads it with LSU loads (valid for peer and local memory alike).
+bool is_ipc_mapped(const void *p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  for (const auto &e : g_ipc) {
+    const uintptr_t b = reinterpret_cast<uintptr_t>(e.base);
+    if (a >= b && a < b + e.size)
+      return true;
+  }
+  return false;
+}
+
 template <class KT> bool aligned_keys(const void *p) {
   return (reinterpret_cast<uintptr_t>(p) % alignof(typename KT::T)) == 0;
 }
@@ -883,8 +933,12 @@ template <class KT> struct SegmentOp {
 // caller's stream, no host synchronisation.
 // Is p memory of another device than `dev` (a peer mapping)?
 bool is_peer(const void *p, int dev) {
+  if (!p)
+    return false;
+  if (is_ipc_mapped(p))
+    return true;
   cudaPointerAttributes at{};
-  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -1635,23 +1689,10 @@ int mp_ipc_export(const void *dev_ptr, void *handle64, uint64_t *offset) {
   g_err.clear();
   if (!dev_ptr || !handle64 || !offset)
     return fail(MP_ERR_INVALID, "ipc_export: NULL argument");
-  // base of the allocation containing dev_ptr: cuMemGetAddressRange via the
-  // runtime's driver entry point (no link-time dependency on libcuda)
-  using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
-  static GetRange get_range = [] {
-    void *fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault,
-                                &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      fn = nullptr;
-    return reinterpret_cast<GetRange>(fn);
-  }();
-  if (!get_range)
-    return fail(MP_ERR_CUDA, "ipc_export: cuMemGetAddressRange unavailable");
-  unsigned long long base = 0;
+  // base of the allocation containing dev_ptr
+  uintptr_t base = 0;
   size_t size = 0;
-  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+  if (!alloc_range(dev_ptr, &base, &size))
     return fail(MP_ERR_INVALID, "ipc_export: not a device allocation");
   cudaIpcMemHandle_t h;
   MP_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
@@ -1663,15 +1704,6 @@ int mp_ipc_export(const void *dev_ptr, void *handle64, uint64_t *offset) {
 // Imported mappings, one per (importing device, allocation handle), with a
 // reference count: every mp_ipc_import takes a reference, mp_ipc_close drops
 // one and unmaps the allocation when the last reference goes.
-struct IpcMapping {
-  int dev;
-  std::string handle;
-  void *base;
-  size_t refs;
-};
-std::mutex g_ipc_mu;
-std::vector<IpcMapping> g_ipc;
-
 int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr) {
   g_err.clear();
   if (!handle64 || !dev_ptr)
@@ -1690,7 +1722,11 @@ int mp_ipc_import(const void *handle64, uint64_t offset, void **dev_ptr) {
   std::memcpy(&h, handle64, sizeof h);
   void *base = nullptr;
   MP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
-  g_ipc.push_back({dev, key, base, 1});
+  uintptr_t rb = 0;
+  size_t rsz = 0;
+  if (!alloc_range(base, &rb, &rsz) || rb != reinterpret_cast<uintptr_t>(base))
+    rsz = 0;  // unknown extent: only the base pointer itself is recognised
+  g_ipc.push_back({dev, key, base, rsz ? rsz : 1, 1});
   *dev_ptr = static_cast<char *>(base) + offset;
   return MP_OK;
 }
@@ -1724,6 +1760,12 @@ int mp_ipc_close(const void *dev_ptr) {
 // system-scope fence (prior work of the stream is visible first); the wait
 // blocks the stream's front end -- no SM is spent spinning.
 namespace {
+__global__ void signal_kernel(unsigned long long *flag, unsigned long long value) {
+  // prior kernels of the stream are complete; order this store after them
+  // for every observer, including peers over NVLink
+  asm volatile("fence.sc.sys;\n\tst.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value)
+               : "memory");
+}
 using StreamValueFn = int (*)(void *, unsigned long long, unsigned long long, unsigned int);
 StreamValueFn driver_fn(const char *name) {
   void *fn = nullptr;
@@ -1742,10 +1784,19 @@ int mp_signal(uint64_t *flag, uint64_t value, void *stream) {
   static const StreamValueFn w = driver_fn("cuStreamWriteValue64");
   if (!flag || (reinterpret_cast<uintptr_t>(flag) & 7))
     return fail(MP_ERR_INVALID, "signal: flag must be an 8-byte aligned device address");
-  if (!w)
-    return fail(MP_ERR_CUDA, "signal: cuStreamWriteValue64 unavailable");
-  if (int e = w(stream, reinterpret_cast<unsigned long long>(flag), value, 0))
-    return fail(MP_ERR_CUDA, "cuStreamWriteValue64 failed (%d)", e);
+  // MP_SIGNAL_KERNEL=1: always the kernel path (tests it on any box)
+  static const bool force_kernel = [] {
+    const char *e = std::getenv("MP_SIGNAL_KERNEL");
+    return e && std::strcmp(e, "1") == 0;
+  }();
+  if (!force_kernel && w && w(stream, reinterpret_cast<unsigned long long>(flag), value, 0) == 0)
+    return MP_OK;
+  // no stream memory operations on this address (e.g. a peer mapping the
+  // driver refuses): one thread stores it, system-scope release
+  cudaGetLastError();
+  signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<unsigned long long *>(flag), value);
+  MP_LAUNCHED("signal_kernel");
   return MP_OK;
 }
 

@@ -226,6 +226,19 @@ def test_p2p_sorter_processes(cuda, sizes):
     assert np.array_equal(got, np.sort(x))
 
 
+def test_signal_kernel_fallback_subprocess(cuda):
+    """mp_signal's kernel fallback (a system-scope release store, used when
+    the driver refuses a stream write to an address) forced on for the
+    multi-process merger and sorter (MP_SIGNAL_KERNEL=1, read once per
+    process)."""
+    import subprocess
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", str(Path(__file__)),
+                        "-k", "p2p_merger or p2p_sorter"], capture_output=True, text=True,
+                       timeout=900, env=dict(os.environ, MP_SIGNAL_KERNEL="1"), cwd=str(ROOT))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 def test_peer_lsu_loader_subprocess(cuda):
     """The peer-memory loader of K2 (LSU vector loads instead of bulk
     copies; chosen for windows on another GPU) forced on for every piece

@@ -17,8 +17,9 @@ phases), so time-slicing the ranks on one GPU is safe.
     sort.hpp:132-148); the concatenated slices equal torch.sort of the keys
     (bare keys: the sorted bytes are unique, so any correct sort is the
     oracle).
-  * both again with MP_PEER_LSU=1 (the LSU peer loader K2 uses for windows
-    on another GPU, forced for every piece merge).
+  * both with the default loader choice (a rank's own shards through the
+    bulk-copy engine, mapped peer shards through LSU loads) and with
+    MP_PEER_LSU=1 (the LSU loader for every window).
 
 The parent process owns the inputs and the output on cuda:0 and hands them
 to the ranks as CUDA tensors (torch.multiprocessing shares them through
@@ -156,7 +157,7 @@ def _gen_sorted_f32(kind, seed, n, dev):
     return x
 
 
-@pytest.mark.parametrize("peer_lsu", [False, True], ids=["bulk", "peer_lsu"])
+@pytest.mark.parametrize("peer_lsu", [False, True], ids=["default", "peer_lsu"])
 def test_config5_eight_ranks_vs_reference(cuda, peer_lsu):
     import torch
     from oracle import bindings as B
@@ -183,7 +184,7 @@ def test_config5_eight_ranks_vs_reference(cuda, peer_lsu):
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-@pytest.mark.parametrize("peer_lsu", [False, True], ids=["bulk", "peer_lsu"])
+@pytest.mark.parametrize("peer_lsu", [False, True], ids=["default", "peer_lsu"])
 def test_config4_sorter_ranks(cuda, world, peer_lsu):
     import torch
     from paper_1406_2628_b200 import _native as N
