@@ -433,8 +433,9 @@ def test_config3_full_size_stability(cuda, variant):
 
 
 def test_config4_sort_full_size(cuda):
-    """Config 4 on one GPU: 2^30 u32 keys, 2048-key block sort + 19 rounds;
-    equals torch.sort of the same keys (bare keys: sorted order is unique)."""
+    """Config 4 on one GPU: 2^30 u32 keys, 16384-key block sort + 16 rounds
+    (8 fused pairs); equals torch.sort of the same keys (bare keys: sorted
+    order is unique)."""
     torch = _torch()
     from paper_1406_2628_b200 import _native as N
     n = 1 << 30
@@ -445,6 +446,29 @@ def test_config4_sort_full_size(cuda):
     N.check(N.lib.mp_sort(N.KEY_U32, x.data_ptr(), None, n, None, 0, st))
     got = x.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
     assert torch.equal(got, ref)
+
+
+def test_config4_sort_full_size_vs_reference(cuda):
+    """Config 4 at full size byte for byte against the REFERENCE's own
+    parallel_merge_sort (oracle/_ref, sort.hpp:132-148, on this host's
+    cores) on the same 2^30 keys -- and the host-span drop-in path
+    (mp_sort_host from pageable memory) gives the same bytes."""
+    torch = _torch()
+    B = _ref_or_skip()
+    from paper_1406_2628_b200 import _native as N
+    n = 1 << 30
+    x = torch.empty(n, dtype=torch.uint32, device=cuda)
+    st = torch.cuda.current_stream().cuda_stream
+    N.check(N.lib.mp_generate(0, 4, 0, n, x.data_ptr(), st))
+    hx = x.cpu().numpy()
+    N.check(N.lib.mp_sort(N.KEY_U32, x.data_ptr(), None, n, None, 0, st))
+    got = x.cpu().numpy()
+    del x
+    want, _ = B.ref().merge_sort("u32", hx, p=B.host_cores())
+    assert got.tobytes() == want.tobytes()
+    ho = np.empty_like(hx)
+    N.check(N.lib.mp_sort_host(N.KEY_U32, hx.ctypes.data, None, n, ho.ctypes.data, None, 0))
+    assert ho.tobytes() == want.tobytes()
 
 
 @pytest.mark.parametrize("kind", ["u32", "i32", "f32"])
