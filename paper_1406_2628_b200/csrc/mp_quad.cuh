@@ -378,31 +378,33 @@ __device__ __forceinline__ int split_predicted(const char *smem, uint32_t oA, in
   return l;
 }
 
-template <class KT, int NT, int VT>
-__global__ void __launch_bounds__(NT, 1536 / NT)
-    quad_tile_kernel(const typename KT::T *__restrict__ src,
-                     typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
-                     uint32_t lg4w, uint32_t T, const QuadPt *__restrict__ Q) {
+// A fused-pass tile's four run windows into smem at kWin0 (K5e's
+// prologue).  The windows travel as whole 16-byte granules: one bulk copy
+// per window covers its unaligned head and tail too (the extra bytes land
+// in the gap before the window and in its sentinel area, which is written
+// after the copy), so thread 0's setup is one dependent load (the split
+// points) and the copy issue -- no edge loads.  Only where a granule would
+// leave the array (its first / last window) are those < 16 bytes read by
+// plain loads.  The other threads wait on the mbarrier for the copies and
+// the header; one barrier at the end orders the sentinel stores.  Returns
+// the windows' offsets and lengths and the tile's first output position.
+struct QuadTileHdr {
+  uint32_t oW[4];
+  int cnt[4];
+  unsigned long long o0;
+};
+
+template <class KT, int VT>
+__device__ __forceinline__ void quad_load_tile(char *smem, const typename KT::T *__restrict__ src,
+                                               uint64_t n, uint64_t w, uint32_t lg4w, uint32_t T,
+                                               const QuadPt *__restrict__ Q, uint32_t (&oW)[4],
+                                               int (&cnt)[4], uint64_t &o0) {
   using T_ = typename KT::T;
   constexpr uint32_t KS = sizeof(T_);
-  extern __shared__ __align__(128) char smem[];
   uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
-  const int tid = threadIdx.x;
-  struct Hdr {
-    uint32_t oW[4];
-    int cnt[4];
-    unsigned long long o0;
-  };
-  Hdr *hdr = reinterpret_cast<Hdr *>(smem + 16);
+  QuadTileHdr *hdr = reinterpret_cast<QuadTileHdr *>(smem + 16);
   constexpr uint32_t kWin0 = 64;
-  // The windows travel as whole 16-byte granules: one bulk copy per window
-  // covers its unaligned head and tail too (the extra bytes land in the gap
-  // before the window and in its sentinel area, which is written after the
-  // copy), so warp 0's setup is one dependent load (the split points) and
-  // the copy issue -- no edge loads.  Only where a granule would leave the
-  // array (its first / last window) are those < 16 bytes read by plain
-  // loads.  The other warps wait on the mbarrier for the copies and the
-  // header, then one barrier orders the sentinel stores.
+  const int tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -460,15 +462,12 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
       }
   }
   mbar_wait(bar, 0);
-  uint32_t oW[4];
-  int cnt[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
     oW[r] = hdr->oW[r];
     cnt[r] = hdr->cnt[r];
   }
-  const uint64_t o0 = hdr->o0;
-  const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
+  o0 = hdr->o0;
   {
     const int w_ = tid >> 5, l = tid & 31;
     if (w_ == 0) {  // sentinels behind the windows (after the copies landed)
@@ -510,6 +509,23 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
     }
   }
   __syncthreads();
+
+}
+
+template <class KT, int NT, int VT>
+__global__ void __launch_bounds__(NT, 1536 / NT)
+    quad_tile_kernel(const typename KT::T *__restrict__ src,
+                     typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
+                     uint32_t lg4w, uint32_t T, const QuadPt *__restrict__ Q) {
+  using T_ = typename KT::T;
+  constexpr uint32_t KS = sizeof(T_);
+  extern __shared__ __align__(128) char smem[];
+  const int tid = threadIdx.x;
+  uint32_t oW[4];
+  int cnt[4];
+  uint64_t o0;
+  quad_load_tile<KT, VT>(smem, src, n, w, lg4w, T, Q, oW, cnt, o0);
+  const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
 
   // ---- phase 1: dynamic split of the threads between X and Y ----
   T_ keys[VT];

@@ -684,3 +684,147 @@ __device__ __forceinline__ int split_after(const char *smem, uint32_t oA, int na
 #define MP_K5E_CHAINS 2
 #endif
 
+
+
+// ===== K5f quad_tile_split_kernel (MP_K5F, round 2): X and Y in their own
+// smem region so both merge phases store each output as produced (no VT
+// output registers, 3 barriers instead of 5), at twice the smem per tile.
+// B200 (tools/ab_k5f.sh, 2^30 sort, 50 steps): K5e 26.28-26.31 ms; K5f at
+// 8192-output tiles 640 x 13, 3 CTAs/SM: 33.13 ms (K5f 2.79 ms per pass at
+// 65 % issue, K4q + K4r 0.36 ms at the 8192 spacing); 448 x 19: 29.66-29.70
+// (2.35 ms); 16384 tiles 1024 x 17, 1 CTA/SM: 39.93.  Not kept.
+// ---------------------------------------------------------------------------
+// K5f: the fused pass with X and Y in their own smem region.  K5e writes X
+// and Y over the input windows and the output over X and Y, so every merge
+// first collects its VT outputs in registers and waits at a barrier before
+// storing them (VT registers per thread, two CTAs of 20 warps per SM).
+// Here the merges store each output as it is produced: phase 1 into the
+// X/Y region, phase 2 into the (dead) input region as the output staging.
+// No output registers, three barriers instead of five -- at the price of
+// twice the smem per tile, so the tile is TILE outputs (8192: three CTAs
+// per SM) and K4q/K4r run at that spacing.
+// ---------------------------------------------------------------------------
+template <class KT, int VT, int TILE>
+__host__ __device__ constexpr uint32_t quad_split_in_bytes() {
+  return ((64 + TILE * sizeof(typename KT::T) + 4 * quad_gap_bytes<KT, VT>() + 64) + 127) & ~127u;
+}
+template <class KT, int VT, int TILE>
+__host__ __device__ constexpr uint32_t quad_split_smem_bytes() {
+  return quad_split_in_bytes<KT, VT, TILE>() + TILE * sizeof(typename KT::T) +
+         (VT + 1) * sizeof(typename KT::T) + 64;
+}
+
+// Serial stable merge of up to VT outputs (bare keys on sentinels) from split
+// (i, j) of the smem windows at oA / oB, each output stored at once to smem
+// offset oOut + k * KS (k < cnt).
+template <class KT, int VT>
+__device__ __forceinline__ void merge_store_smem(char *smem, uint32_t oA, uint32_t oB, int i,
+                                                 int j, uint32_t oOut, int cnt) {
+  using T = typename KT::T;
+  constexpr uint32_t KS = sizeof(T);
+  uint32_t pa = oA + i * KS, pb = oB + j * KS;
+  T ka = lds<T>(smem, pa), kb = lds<T>(smem, pb);
+  if (cnt >= VT) {
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+      const bool tb = take_b<KT>(kb, ka);
+      *reinterpret_cast<T *>(smem + oOut + k * KS) = tb ? kb : ka;
+      pa += tb ? 0u : KS;
+      pb += tb ? KS : 0u;
+      const T nxt = lds<T>(smem, tb ? pb : pa);
+      kb = tb ? nxt : kb;
+      ka = tb ? ka : nxt;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < VT; ++k) {
+      if (k >= cnt)
+        break;
+      const bool tb = take_b<KT>(kb, ka);
+      *reinterpret_cast<T *>(smem + oOut + k * KS) = tb ? kb : ka;
+      pa += tb ? 0u : KS;
+      pb += tb ? KS : 0u;
+      const T nxt = lds<T>(smem, tb ? pb : pa);
+      kb = tb ? nxt : kb;
+      ka = tb ? ka : nxt;
+    }
+  }
+}
+
+template <class KT, int NT, int VT, int TILE, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    quad_tile_split_kernel(const typename KT::T *__restrict__ src,
+                           typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
+                           uint32_t lg4w, const QuadPt *__restrict__ Q) {
+  using T_ = typename KT::T;
+  constexpr uint32_t KS = sizeof(T_);
+  static_assert(NT * VT >= TILE + 2 * VT && (VT & 1), "K5f shape");
+  extern __shared__ __align__(128) char smem[];
+  const int tid = threadIdx.x;
+  uint32_t oW[4];
+  int cnt[4];
+  uint64_t o0;
+  quad_load_tile<KT, VT>(smem, src, n, w, lg4w, TILE, Q, oW, cnt, o0);
+  const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
+  // X and Y (plus their sentinels) in their own region
+  constexpr uint32_t XY0 = quad_split_in_bytes<KT, VT, TILE>();
+  const uint32_t oX = XY0;
+  const uint32_t oY = (oX + (nx + VT) * KS + 15u) & ~15u;
+
+  // ---- phase 1: X = merge(R0w, R1w), Y = merge(R2w, R3w), stored at once ----
+  {
+    const int tx = (nx + VT - 1) / VT;
+    const int side = tid >= tx ? 1 : 0;
+    const int t1 = tid - side * tx;
+    const uint32_t oA = side ? oW[2] : oW[0], oB = side ? oW[3] : oW[1];
+    const int na = side ? cnt[2] : cnt[0], nb = side ? cnt[3] : cnt[1];
+    const int d1 = t1 * VT;
+    if (d1 < na + nb) {
+      const int lo = split_predicted<KT, MP_QUAD_PRED_LOGW>(
+          smem, oA, na, oB, nb, d1, static_cast<float>(na) / static_cast<float>(na + nb));
+      merge_store_smem<KT, VT>(smem, oA, oB, lo, d1 - lo, (side ? oY : oX) + d1 * KS,
+                               na + nb - d1);
+    }
+    if (tid >= NT - 32) {  // the last warp: X's VT sentinels and Y's one
+      const int l = tid - (NT - 32);
+      if (l < VT)
+        *reinterpret_cast<T_ *>(smem + oX + (nx + l) * KS) = KT::max_key();
+      else if (l == VT)
+        *reinterpret_cast<T_ *>(smem + oY + ny * KS) = KT::max_key();
+    }
+  }
+  __syncthreads();  // X and Y complete; the input windows are dead
+
+  // ---- phase 2: out = merge(X, Y), ties to X, staged over the input region ----
+  T_ *out = dst + o0;
+  const uint32_t oS = mirror_off(16, out);
+  uint32_t olo;
+  const uint32_t oib = interior_bytes(reinterpret_cast<const char *>(out),
+                                      static_cast<uint32_t>(total) * KS, &olo);
+  const int d2 = tid * VT;
+  if (d2 < total) {
+    const int lo = split_predicted<KT, MP_QUAD_PRED_LOGW>(
+        smem, oX, nx, oY, ny, d2, static_cast<float>(nx) / static_cast<float>(total));
+    merge_store_smem<KT, VT>(smem, oX, oY, lo, d2 - lo, oS + d2 * KS, total - d2);
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (tid == 0 && oib) {
+    bulk_s2g(reinterpret_cast<char *>(out) + olo, smem + oS + olo, oib);
+    bulk_commit();
+  }
+  if (tid >= 32 && tid < 64) {  // unaligned head / tail (< 16 B each)
+    const uint32_t bytes = static_cast<uint32_t>(total) * KS;
+    const uint32_t hi = oib ? olo + oib : bytes;
+    const uint32_t hlo = oib ? olo : bytes;
+    const uint32_t nh = hlo / KS, nt = (bytes - hi) / KS;
+    const uint32_t l = tid - 32;
+    if (l < nh + nt) {
+      const uint32_t e = l < nh ? l : (hi / KS) + (l - nh);
+      out[e] = lds<T_>(smem, oS + e * KS);
+    }
+  }
+  if (tid == 0 && oib)
+    bulk_wait_read0();
+}
+
