@@ -206,8 +206,8 @@ typedef struct mp_shard {
  * positions [len(out[0..g)), + out[g].len) and is computed ON out[g].device,
  * its windows read straight from the input shards' devices (peer access is
  * enabled; NVLink pull inside the tile loads).  sum(out.len) must equal
- * |A| + |B| (parallel.hpp:155-156).  Values ride along when out[0].vals is
- * non-NULL (then every non-empty shard carries them).
+ * |A| + |B| (parallel.hpp:155-156).  Values ride along when any output
+ * shard has a vals pointer (then every non-empty shard carries them).
  * streams == NULL: blocking (all involved devices synchronised at entry,
  * the call returns when the output is complete).  Otherwise streams[g] (on
  * out[g].device) for each output shard: asynchronous, ordered after all
@@ -216,7 +216,7 @@ typedef struct mp_shard {
 int mp_multi_merge(int key_type, const mp_shard *a, int na, const mp_shard *b, int nb,
                    const mp_shard *out, int nout, void *const *streams);
 /* In-place stable sort of X = x[0] ++ ... ++ x[P-1] (P = 1..16 shards, any
- * devices; values ride along when x[0].vals is non-NULL): afterwards x[g]
+ * devices; values ride along when any shard has a vals pointer): afterwards x[g]
  * holds sorted positions [len(x[0..g)), + x[g].len).  Each shard is sorted
  * on its device (mp_sort), then ceil(log2 P) rounds merge rank groups
  * (left group = A: stable w.r.t. the input order) with every shard keeping

@@ -114,6 +114,15 @@ struct MultiCtx {
   }
 };
 
+// values ride along when any shard of the table carries them (an empty
+// shard may have no value pointer)
+bool any_vals(const mp_shard *x, int n) {
+  for (int g = 0; g < n; ++g)
+    if (x[g].vals)
+      return true;
+  return false;
+}
+
 int check_shards(const mp_shard *x, int n, const char *what, bool vals_all) {
   if (n < 1 || n > kMaxPieces)
     return fail(MP_ERR_INVALID, "multi: 1..%d %s shards", kMaxPieces, what);
@@ -134,7 +143,9 @@ int check_shards(const mp_shard *x, int n, const char *what, bool vals_all) {
 template <class KT> struct MultiMergeOp {
   static int run(const mp_shard *a, int na, const mp_shard *b, int nb, const mp_shard *o,
                  int no, void *const *streams) {
-    const bool vals = o[0].vals != nullptr;
+    if (no < 1 || no > kMaxPieces)
+      return fail(MP_ERR_INVALID, "multi: 1..%d out shards", kMaxPieces);
+    const bool vals = any_vals(o, no);
     if (int rc = check_shards(a, na, "A", vals))
       return rc;
     if (int rc = check_shards(b, nb, "B", vals))
@@ -182,7 +193,9 @@ template <class KT> struct MultiMergeOp {
 template <class KT> struct MultiSortOp {
   static int run(const mp_shard *x, int P, void *const *streams) {
     using T = typename KT::T;
-    const bool vals = x[0].vals != nullptr;
+    if (P < 1 || P > kMaxPieces)
+      return fail(MP_ERR_INVALID, "multi: 1..%d sort shards", kMaxPieces);
+    const bool vals = any_vals(x, P);
     if (int rc = check_shards(x, P, "sort", vals))
       return rc;
     if (vals && KT::kind == kElement)

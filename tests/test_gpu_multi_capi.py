@@ -78,3 +78,40 @@ def test_multi_sort_and_merge_key_types(cuda, port, S):
                                  N.shards_array(to), 3, None))
     m, _, _, _ = port.merge(S, want[:h], want[h:])
     assert torch.cat(ko).cpu().numpy().view(m.dtype).tobytes() == m.tobytes()
+
+
+def test_multi_sort_values_with_empty_first_shard(cuda, port):
+    """Values ride along when ANY shard carries them -- an empty first shard
+    has no value pointer (regression found by tools/stress_multi.py)."""
+    import torch
+    from paper_1406_2628_b200 import _native as N
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, 7, 301).astype(np.uint32)
+    v = np.arange(301, dtype=np.uint32)
+    want, wantv, _ = port.merge_sort("u32", x, vals=v)
+    cuts = [0, 0, 2, 150, 301]
+    keys = [torch.from_numpy(x[cuts[g]:cuts[g + 1]].copy()).to(cuda) for g in range(4)]
+    vals = [torch.from_numpy(v[cuts[g]:cuts[g + 1]].copy()).to(cuda) for g in range(4)]
+    tab = [(0, k.data_ptr() if k.numel() else None, w.data_ptr() if w.numel() else None,
+            k.numel()) for k, w in zip(keys, vals)]
+    N.check(N.lib.mp_multi_sort(N.KEY_U32, N.shards_array(tab), 4, None))
+    assert np.array_equal(torch.cat(keys).cpu().numpy(), want)
+    assert np.array_equal(torch.cat(vals).cpu().numpy(), wantv)
+    # the same table through the merge: A = the sorted first half, B = the rest
+    h = 150
+    a_k = [torch.from_numpy(want[:h].copy()).to(cuda)]
+    b_k = [torch.from_numpy(want[h:].copy()).to(cuda)]
+    a_v = [torch.from_numpy(np.arange(h, dtype=np.uint32)).to(cuda)]
+    b_v = [torch.from_numpy(np.arange(301 - h, dtype=np.uint32) | np.uint32(1 << 31)).to(cuda)]
+    out_k = [torch.empty(0, dtype=torch.uint32, device=cuda),
+             torch.empty(301, dtype=torch.uint32, device=cuda)]
+    out_v = [torch.empty(0, dtype=torch.uint32, device=cuda),
+             torch.empty(301, dtype=torch.uint32, device=cuda)]
+    N.check(N.lib.mp_multi_merge(
+        N.KEY_U32, N.shards_array([(0, a_k[0].data_ptr(), a_v[0].data_ptr(), h)]), 1,
+        N.shards_array([(0, b_k[0].data_ptr(), b_v[0].data_ptr(), 301 - h)]), 1,
+        N.shards_array([(0, None, None, 0), (0, out_k[1].data_ptr(), out_v[1].data_ptr(), 301)]),
+        2, None))
+    m, mv, _, _ = port.merge("u32", want[:h], want[h:], av=a_v[0].cpu().numpy(),
+                             bv=b_v[0].cpu().numpy())
+    assert np.array_equal(out_k[1].cpu().numpy(), m) and np.array_equal(out_v[1].cpu().numpy(), mv)
