@@ -267,7 +267,8 @@ constexpr int kBigTileNT = 384;       // 384 x 23 >= 8192
 // 8192-output tile 384 x 23 29.49 ms, 288 x 31 29.11, 320 x 27 29.01; at
 // the 16384-output tile 640 x 27 28.17-28.32 (K4q + K4r per pass 0.39 ->
 // 0.18 ms, K5e 2.07 -> 2.13 ms), 544 x 31 29.28, 576 x 29 28.14, 704 x 25
-// 28.54
+// 28.54.  Round 2, after the granule copies (tools/ab_qshape2.sh, 2^30
+// sort): 640 x 27 26.27, 576 x 29 26.25, 672 x 25 26.52, 704 x 25 28.49 ms.
 #ifndef MP_QUAD_NT
 #define MP_QUAD_NT 640
 #endif
