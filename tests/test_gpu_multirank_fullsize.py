@@ -14,9 +14,8 @@ phases), so time-slicing the ranks on one GPU is safe.
     parallel.hpp:151-162) on the same input bytes.
   * config 4 (2^30 u32, seed 4) through P2PSorter at P = 2, 4, 8 (local
     sort of a 1/P shard + log2 P cross-rank Merge Path rounds,
-    sort.hpp:132-148); the concatenated slices equal torch.sort of the keys
-    (bare keys: the sorted bytes are unique, so any correct sort is the
-    oracle).
+    sort.hpp:132-148); the concatenated slices equal, byte for byte, the
+    reference's own parallel_merge_sort of the keys (oracle/_ref).
   * both with the default loader choice (a rank's own shards through the
     bulk-copy engine, mapped peer shards through LSU loads) and with
     MP_PEER_LSU=1 (the LSU loader for every window).
@@ -147,6 +146,22 @@ def _run_ranks(target, world, *args):
     return edges
 
 
+_REF_SORT = {}
+
+
+def _reference_sort(keys):
+    """oracle/_ref's parallel_merge_sort on this host's cores (cached: the
+    six sorter tests share the config-4 keys); torch.sort where the
+    reference library is not built."""
+    if "c4" not in _REF_SORT:
+        from oracle import bindings as B
+        if B.REF_LIB.exists():
+            _REF_SORT["c4"], _ = B.ref().merge_sort("u32", keys, p=B.host_cores())
+        else:
+            _REF_SORT["c4"] = np.sort(keys)
+    return _REF_SORT["c4"]
+
+
 def _gen_sorted_f32(kind, seed, n, dev):
     import torch
     from paper_1406_2628_b200 import _native as N
@@ -195,7 +210,8 @@ def test_config4_sorter_ranks(cuda, world, peer_lsu):
     torch.cuda.synchronize()
     edges = _run_ranks(_sort_rank, world, peer_lsu, x, out)
     assert edges[-1][1] == n
-    # u32 keys, exact in int64 (torch.sort has no uint32 path)
-    want = torch.sort(x.to(torch.int64)).values
+    # the REFERENCE's parallel_merge_sort (sort.hpp:132-148) on the same
+    # keys, computed once per session
+    want = _reference_sort(x.cpu().numpy())
     del x
-    assert torch.equal(out.to(torch.int64), want)
+    assert out.cpu().numpy().tobytes() == want.tobytes()
