@@ -404,3 +404,14 @@ __device__ __forceinline__ uint32_t lds_padded(uint32_t base, uint32_t k) {
       ka = tb ? ka : nx;
     }
 #endif
+
+// ===== K3w passes with FMA-pipe smem addressing (MP_K3W_FMA_ADDR, round 2):
+// every padded LDS address of the split searches and merge loops formed by
+// mul.hi / mad.lo (IMAD.HI / IMAD) instead of LEA.HI / LEA.  B200
+// (tools/ab_k3w_fma.sh, 512 x 32): ALU pipe 80 -> 74 %, FMA 14 %, but K3w
+// 8.05 -> 8.19 ms and the sort 26.27 -> 26.42 ms (a three-deep IMAD chain
+// on every load).  Not kept.
+//   uint32_t h, a;  // k -> shared address of padded word k
+//   asm("mul.hi.u32 %0, %1, 134217728;" : "=r"(h) : "r"(k));
+//   asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a) : "r"(k), "r"(base));
+//   asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(a) : "r"(h), "r"(a));
