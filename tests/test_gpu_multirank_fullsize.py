@@ -16,7 +16,9 @@ phases), so time-slicing the ranks on one GPU is safe.
     sort of a 1/P shard + log2 P cross-rank Merge Path rounds,
     sort.hpp:132-148); the concatenated slices equal, byte for byte, the
     reference's own parallel_merge_sort of the keys (oracle/_ref).
-  * both with the default loader choice (a rank's own shards through the
+  * config 3a (u64 keys + u32 values, 2^29 + 2^25) as 8 ranks: keys and
+    values byte-compared with the reference's {key, value} merge.
+  * all with the default loader choice (a rank's own shards through the
     bulk-copy engine, mapped peer shards through LSU loads) and with
     MP_PEER_LSU=1 (the LSU loader for every window).
 
@@ -86,6 +88,32 @@ def _merge_rank(rank, world, port, peer_lsu, a_all, b_all, out_all, q):
         out, _ = m()
         assert out.numel() == m.o1 - m.o0
         out_all[m.o0:m.o1].copy_(out)
+        torch.cuda.synchronize()
+        m.close()
+        dist.barrier()
+        q.put((rank, "ok", (m.o0, m.o1)))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, "ERR", traceback.format_exc()))
+
+
+def _merge_vals_rank(rank, world, port, peer_lsu, a_all, b_all, av_all, bv_all, out_all,
+                     outv_all, q):
+    try:
+        torch, dist = _rank_env(rank, world, port, peer_lsu)
+        from paper_1406_2628_b200 import _native as N
+        from paper_1406_2628_b200 import multigpu as mg
+        na, nb = a_all.numel(), b_all.numel()
+        sa = slice(rank * na // world, (rank + 1) * na // world)
+        sb = slice(rank * nb // world, (rank + 1) * nb // world)
+        a, av = a_all[sa].clone(), av_all[sa].clone()
+        b, bv = b_all[sb].clone(), bv_all[sb].clone()
+        torch.cuda.synchronize()
+        m = mg.P2PMerger(a, b, av, bv, key_type=N.KEY_U64)
+        out, outv = m()
+        out_all[m.o0:m.o1].copy_(out)
+        outv_all[m.o0:m.o1].copy_(outv)
         torch.cuda.synchronize()
         m.close()
         dist.barrier()
@@ -215,3 +243,43 @@ def test_config4_sorter_ranks(cuda, world, peer_lsu):
     want = _reference_sort(x.cpu().numpy())
     del x
     assert out.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_config3a_values_eight_ranks_vs_reference(cuda):
+    """Config 3a (u64 keys + u32 values = source index, bit 31 marks B;
+    |A| = 2^29, |B| = 2^25) as 8 ranks: keys and values byte-compared with
+    the reference's parallel_merge_into on {key, value} records (stability
+    across rank boundaries is visible in the values)."""
+    import torch
+    from oracle import bindings as B
+    from paper_1406_2628_b200 import _native as N
+    if not B.REF_LIB.exists():
+        pytest.skip("oracle/_ref (the reference library) not built")
+    st = torch.cuda.current_stream().cuda_stream
+    na, nb = 1 << 29, 1 << 25
+
+    def gen(seed, n):
+        x = torch.empty(n, dtype=torch.uint64, device=cuda)
+        N.check(N.lib.mp_generate(2, seed, 0, n, x.data_ptr(), st))
+        N.check(N.lib.mp_sort(N.KEY_U64, x.data_ptr(), None, n, None, 0, st))
+        return x
+
+    a, b = gen(1, na), gen(2, nb)
+    av = torch.arange(na, dtype=torch.int32, device=cuda).view(torch.uint32)
+    bv = (torch.arange(nb, dtype=torch.int32, device=cuda)
+          + torch.iinfo(torch.int32).min).view(torch.uint32)
+    out = torch.zeros(na + nb, dtype=torch.uint64, device=cuda)
+    outv = torch.zeros(na + nb, dtype=torch.uint32, device=cuda)
+    torch.cuda.synchronize()
+    _run_ranks(_merge_vals_rank, 8, False, a, b, av, bv, out, outv)
+    ra = np.zeros(na, dtype=B.KV_DTYPE)
+    ra["key"], ra["val"] = a.cpu().numpy(), av.cpu().numpy()
+    rb = np.zeros(nb, dtype=B.KV_DTYPE)
+    rb["key"], rb["val"] = b.cpu().numpy(), bv.cpu().numpy()
+    del a, b, av, bv
+    got, gotv = out.cpu().numpy(), outv.cpu().numpy()
+    del out, outv
+    team = B.ref().team(B.host_cores())
+    want, _, _ = B.ref().merge("kv", ra, rb, team=team)
+    team.close()
+    assert np.array_equal(got, want["key"]) and np.array_equal(gotv, want["val"])
