@@ -35,6 +35,7 @@ place of the device kernels.
 from __future__ import annotations
 
 import bisect
+from ctypes import c_void_p as C_void_p
 from dataclasses import dataclass
 
 import torch
@@ -784,6 +785,54 @@ def nvlink_probe(comm, device, mib=1024, reps=5):
     allr = comm.all_gather_int([int(mine * 1000)])
     per_rank = [x[0] / 1000 for x in allr]
     return per_rank, min(per_rank)
+
+
+# --------------------------------------------------------------------------
+# one process, several GPUs: the shard-table C ABI (mp_multi_merge / _sort)
+# --------------------------------------------------------------------------
+def _shard_table(keys, vals, kt):
+    rows = []
+    for k, v in zip(keys, vals if vals is not None else [None] * len(keys)):
+        if not k.is_cuda:
+            raise ValueError("shards must be CUDA tensors")
+        n = n_keys(k, kt)
+        rows.append((k.device.index, k.data_ptr() if n else None,
+                     v.data_ptr() if v is not None and n else None, n))
+    return N.shards_array(rows), len(rows)
+
+
+def multi_sort(shards, vals=None, key_type=None, streams=None):
+    """Stable in-place sort of the sequence shards[0] ++ shards[1] ++ ...
+    (CUDA tensors on any devices of this process, 1..16 of them; `vals`
+    optional uint32 tensors alongside): afterwards shards[g] holds its slice
+    of the sorted sequence (mp_multi_sort: local sorts, then Merge Path
+    rounds between device groups over NVLink).  Blocking unless `streams`
+    (one torch stream per shard) is given."""
+    kt = key_type_of(shards[0], key_type)
+    tab, n = _shard_table(shards, vals, kt)
+    st = None
+    if streams is not None:
+        st = (C_void_p * n)(*[s.cuda_stream for s in streams])
+    N.check(N.lib.mp_multi_sort(kt, tab, n, st))
+    return shards
+
+
+def multi_merge(a_shards, b_shards, out_shards, a_vals=None, b_vals=None, out_vals=None,
+                key_type=None, streams=None):
+    """Stable merge of A = a_shards[0] ++ ... and B = b_shards[0] ++ ...
+    (ties: A first) into out_shards (their lengths sum to |A| + |B|); each
+    output shard is computed on its own device, reading the inputs over
+    NVLink (mp_multi_merge).  Blocking unless `streams` (one per output
+    shard) is given."""
+    kt = key_type_of(a_shards[0], key_type)
+    ta, na = _shard_table(a_shards, a_vals, kt)
+    tb, nb = _shard_table(b_shards, b_vals, kt)
+    to, no = _shard_table(out_shards, out_vals, kt)
+    st = None
+    if streams is not None:
+        st = (C_void_p * no)(*[s.cuda_stream for s in streams])
+    N.check(N.lib.mp_multi_merge(kt, ta, na, tb, nb, to, no, st))
+    return out_shards
 
 
 # --------------------------------------------------------------------------

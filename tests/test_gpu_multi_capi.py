@@ -115,3 +115,31 @@ def test_multi_sort_values_with_empty_first_shard(cuda, port):
     m, mv, _, _ = port.merge("u32", want[:h], want[h:], av=a_v[0].cpu().numpy(),
                              bv=b_v[0].cpu().numpy())
     assert np.array_equal(out_k[1].cpu().numpy(), m) and np.array_equal(out_v[1].cpu().numpy(), mv)
+
+
+def test_python_multi_sort_and_merge(cuda, port):
+    """multigpu.multi_sort / multi_merge (the shard-table ABI from Python),
+    with values and per-shard streams."""
+    import torch
+    from paper_1406_2628_b200 import multigpu as mg
+    rng = np.random.default_rng(8)
+    x = rng.integers(0, 1000, 500_003).astype(np.int32)
+    v = np.arange(len(x), dtype=np.uint32)
+    want, wantv, _ = port.merge_sort("i32", x, vals=v)
+    cuts = [0, 7, 250_000, 250_001, len(x)]
+    ks = [torch.from_numpy(x[cuts[g]:cuts[g + 1]].copy()).to(cuda) for g in range(4)]
+    vs = [torch.from_numpy(v[cuts[g]:cuts[g + 1]].copy()).to(cuda) for g in range(4)]
+    streams = [torch.cuda.Stream(cuda) for _ in range(4)]
+    mg.multi_sort(ks, vals=vs, streams=streams)
+    for s in streams:
+        s.synchronize()
+    assert np.array_equal(torch.cat(ks).cpu().numpy(), want)
+    assert np.array_equal(torch.cat(vs).cpu().numpy(), wantv)
+    h = 123_456
+    a = [torch.from_numpy(want[:h].copy()).to(cuda)]
+    b = [torch.from_numpy(want[h:h + 1000].copy()).to(cuda),
+         torch.from_numpy(want[h + 1000:].copy()).to(cuda)]
+    out = [torch.empty(n, dtype=torch.int32, device=cuda) for n in (1, len(want) - 1)]
+    mg.multi_merge(a, b, out)
+    m, _, _, _ = port.merge("i32", want[:h], want[h:])
+    assert np.array_equal(torch.cat(out).cpu().numpy(), m)
