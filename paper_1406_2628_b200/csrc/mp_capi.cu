@@ -646,13 +646,13 @@ int sort_impl(const void *in_, const uint32_t *inv, void *keys_,
       if (whole) {
         auto kern = block_sort_warp_kernel<KT, kWarpNT, true, kWarpVT>;
         MP_CUDA(set_smem(kern, smem));
-        kern<<<static_cast<unsigned>(whole), kWarpNT, smem, s>>>(in, src, n, 0);
+        kern<<<static_cast<unsigned>(whole), kWarpNT, smem, s>>>(in, src, n, 0, 1u);
         MP_LAUNCHED("block_sort_warp_kernel");
       }
       if (blocks > whole) {
         auto kern = block_sort_warp_kernel<KT, kWarpNT, false, kWarpVT>;
         MP_CUDA(set_smem(kern, smem));
-        kern<<<static_cast<unsigned>(blocks - whole), kWarpNT, smem, s>>>(in, src, n, whole);
+        kern<<<static_cast<unsigned>(blocks - whole), kWarpNT, smem, s>>>(in, src, n, whole, 1u);
         MP_LAUNCHED("block_sort_warp_kernel(tail)");
       }
     }

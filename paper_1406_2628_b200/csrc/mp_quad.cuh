@@ -471,12 +471,14 @@ __device__ __forceinline__ void quad_load_tile(char *smem, const typename KT::T 
   {
     const int w_ = tid >> 5, l = tid & 31;
     if (w_ == 0) {  // sentinels behind the windows (after the copies landed)
-      if (l < VT) {
-        *reinterpret_cast<T_ *>(smem + oW[0] + (cnt[0] + l) * KS) = KT::max_key();
-        *reinterpret_cast<T_ *>(smem + oW[2] + (cnt[2] + l) * KS) = KT::max_key();
-      } else if (l == VT) {
-        *reinterpret_cast<T_ *>(smem + oW[1] + cnt[1] * KS) = KT::max_key();
-        *reinterpret_cast<T_ *>(smem + oW[3] + cnt[3] * KS) = KT::max_key();
+      for (int k = l; k <= VT; k += 32) {
+        if (k < VT) {
+          *reinterpret_cast<T_ *>(smem + oW[0] + (cnt[0] + k) * KS) = KT::max_key();
+          *reinterpret_cast<T_ *>(smem + oW[2] + (cnt[2] + k) * KS) = KT::max_key();
+        } else {
+          *reinterpret_cast<T_ *>(smem + oW[1] + cnt[1] * KS) = KT::max_key();
+          *reinterpret_cast<T_ *>(smem + oW[3] + cnt[3] * KS) = KT::max_key();
+        }
       }
     } else if (w_ == 1) {  // window edges a granule would have read outside the array
       const int r = l >> 3, e = l & 7;
@@ -512,19 +514,14 @@ __device__ __forceinline__ void quad_load_tile(char *smem, const typename KT::T 
 
 }
 
+// K5e's two merge phases over the loaded windows
 template <class KT, int NT, int VT>
-__global__ void __launch_bounds__(NT, 1536 / NT)
-    quad_tile_kernel(const typename KT::T *__restrict__ src,
-                     typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
-                     uint32_t lg4w, uint32_t T, const QuadPt *__restrict__ Q) {
+__device__ __forceinline__ void quad_tile_merge(char *smem, typename KT::T *__restrict__ dst,
+                                                const uint32_t (&oW)[4], const int (&cnt)[4],
+                                                uint64_t o0) {
   using T_ = typename KT::T;
   constexpr uint32_t KS = sizeof(T_);
-  extern __shared__ __align__(128) char smem[];
   const int tid = threadIdx.x;
-  uint32_t oW[4];
-  int cnt[4];
-  uint64_t o0;
-  quad_load_tile<KT, VT>(smem, src, n, w, lg4w, T, Q, oW, cnt, o0);
   const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
 
   // ---- phase 1: dynamic split of the threads between X and Y ----
@@ -561,11 +558,12 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
     }
   }
   if (tid >= NT - 32) {  // the last warp: X's VT sentinels and Y's one
-    const int l = tid - (NT - 32);
-    if (l < VT)
-      *reinterpret_cast<T_ *>(smem + oX + (nx + l) * KS) = KT::max_key();
-    else if (l == VT)
-      *reinterpret_cast<T_ *>(smem + oY + ny * KS) = KT::max_key();
+    for (int l = tid - (NT - 32); l <= VT; l += 32) {
+      if (l < VT)
+        *reinterpret_cast<T_ *>(smem + oX + (nx + l) * KS) = KT::max_key();
+      else
+        *reinterpret_cast<T_ *>(smem + oY + ny * KS) = KT::max_key();
+    }
   }
   __syncthreads();
 
@@ -612,6 +610,19 @@ __global__ void __launch_bounds__(NT, 1536 / NT)
   }
   if (tid == 0 && ib)
     bulk_wait_read0();
+}
+
+template <class KT, int NT, int VT>
+__global__ void __launch_bounds__(NT, 1536 / NT)
+    quad_tile_kernel(const typename KT::T *__restrict__ src,
+                     typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
+                     uint32_t lg4w, uint32_t T, const QuadPt *__restrict__ Q) {
+  extern __shared__ __align__(128) char smem[];
+  uint32_t oW[4];
+  int cnt[4];
+  uint64_t o0;
+  quad_load_tile<KT, VT>(smem, src, n, w, lg4w, T, Q, oW, cnt, o0);
+  quad_tile_merge<KT, NT, VT>(smem, dst, oW, cnt, o0);
 }
 
 }  // namespace mpb

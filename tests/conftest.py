@@ -59,6 +59,20 @@ def cuda():
     return torch.device("cuda", 0)
 
 
+@pytest.fixture(autouse=True)
+def _release_torch_cache():
+    """The library allocates scratch from its own CUDA pool, which cannot
+    reuse blocks torch's caching allocator keeps after a test (a full-size
+    torch.sort leaves tens of GB cached): hand them back after every test so
+    a later mp_sort / mp_merge never sees an out-of-memory that only the
+    suite's order caused."""
+    yield
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+
 def element_array(keys, tag_base=0):
     from oracle.bindings import ELEMENT_DTYPE
     e = np.zeros(len(keys), dtype=ELEMENT_DTYPE)

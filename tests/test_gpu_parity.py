@@ -443,6 +443,7 @@ def test_config4_sort_full_size(cuda):
     st = torch.cuda.current_stream().cuda_stream
     N.check(N.lib.mp_generate(0, 4, 0, n, x.data_ptr(), st))
     ref = torch.sort(x.view(torch.int32).to(torch.int64) & 0xFFFFFFFF).values
+    torch.cuda.empty_cache()  # torch.sort's temporaries (tens of GB) back to the driver
     N.check(N.lib.mp_sort(N.KEY_U32, x.data_ptr(), None, n, None, 0, st))
     got = x.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
     assert torch.equal(got, ref)

@@ -1,0 +1,232 @@
+// k3w_lab.cu -- A/B bench of compare-exchange encodings for the K3w block
+// sort (mp_bsort.cuh).  B200 pipes (B300_MICROARCH.md "Pipe rates"): ALU and
+// FMA pipes each take a warp instruction every 2 cycles per SMSP; VIMNMX
+// occupies the ALU pipe for 4.  K3w is a pure VIMNMX stream (ncu: ALU 80-90 %),
+// so the lab moves half of every compare-exchange to the FMA pipe:
+//   REG mode 0: lo = min(x,y); hi = max(x,y)                 (2 VIMNMX, 8 ALU)
+//   REG mode 1: lo = min(x,y); hi = x ^ y ^ lo               (VIMNMX + LOP3, 6 ALU)
+//   REG mode 2: lo = min(x,y); hi = (x*one + y) + lo*mone    (VIMNMX + 2 IMAD, 4 ALU + 4 FMA)
+//   REG mode 3: mix of 2 and 1 by comparator parity
+//   LANE mode 0: x = upper ? max(x,y) : min(x,y)             (VIMNMX, 4 ALU)
+//   LANE mode 1: p = (y < x) ^ upper; @p mov x, y            (ISETP + predicated move; ptxas makes it SEL)
+//   LANE mode 2: p = (y < x) ^ upper; @p x = y*one + 0       (ISETP + predicated IMAD, 2 ALU + 2 FMA)
+// Build:  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+//         -I paper_1406_2628_b200/csrc -o tools/bin/k3w_lab tools/k3w_lab.cu
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+#include "mp_bsort.cuh"
+
+using namespace mpb;
+
+template <int RM>
+__device__ __forceinline__ void ce_reg(uint32_t &x, uint32_t &y, uint32_t one, uint32_t mone, int parity) {
+  const uint32_t lo = min(x, y);
+  if constexpr (RM == 0) {
+    y = max(x, y);
+  } else if constexpr (RM == 1) {
+    y = x ^ y ^ lo;
+  } else if constexpr (RM == 2) {
+    uint32_t s, h;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(x), "r"(one), "r"(y));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(lo), "r"(mone), "r"(s));
+    y = h;
+  } else if constexpr (RM == 4 || RM == 5 || RM == 6) {
+    constexpr int K = RM == 4 ? 4 : RM == 5 ? 3 : 2;
+    if (parity % K == 0) {
+      uint32_t s, h;
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(x), "r"(one), "r"(y));
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(lo), "r"(mone), "r"(s));
+      y = h;
+    } else {
+      y = max(x, y);
+    }
+  } else {
+    if (parity & 1) {
+      y = x ^ y ^ lo;
+    } else {
+      uint32_t s, h;
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(s) : "r"(x), "r"(one), "r"(y));
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(h) : "r"(lo), "r"(mone), "r"(s));
+      y = h;
+    }
+  }
+  x = lo;
+}
+
+template <int LM>
+__device__ __forceinline__ void ce_lane(uint32_t &x, uint32_t y, bool upper, uint32_t upper_u, uint32_t one) {
+  if constexpr (LM == 0) {
+    x = upper ? max(x, y) : min(x, y);
+  } else if constexpr (LM == 3) {  // timing only: shuffle + 1 LOP3 (wrong result)
+    x ^= y;
+  } else if constexpr (LM == 2) {
+    asm("{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.u32 q, %2, 0;\n\t"
+        "setp.lt.xor.u32 p, %1, %0, q;\n\t"
+        "@p mad.lo.u32 %0, %1, %3, 0;\n\t}"
+        : "+r"(x)
+        : "r"(y), "r"(upper_u), "r"(one));
+  } else {
+    asm("{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.u32 q, %2, 0;\n\t"
+        "setp.lt.xor.u32 p, %1, %0, q;\n\t"
+        "@p mov.u32 %0, %1;\n\t}"
+        : "+r"(x)
+        : "r"(y), "r"(upper_u));
+  }
+}
+
+template <int N, int RM>
+__device__ __forceinline__ void batcher_lab(uint32_t (&x)[N], uint32_t one, uint32_t mone) {
+  constexpr BatcherNet<N> net{};
+#pragma unroll
+  for (int m = 0; m < net.n; ++m)
+    ce_reg<RM>(x[net.a[m]], x[net.b[m]], one, mone, m);
+}
+
+template <int NT, int VT, int RM, int LM, int PASSES>
+__global__ void __launch_bounds__(NT, 1024 / NT)
+    lab_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint32_t one_) {
+  constexpr int NV = NT * VT;
+  extern __shared__ __align__(128) uint32_t s[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint64_t base = uint64_t(blockIdx.x) * NV;
+  const uint32_t one = one_, mone = 0u - one_;
+  uint32_t x[VT];
+  const uint4 *src = reinterpret_cast<const uint4 *>(in + base);
+#pragma unroll
+  for (int m = 0; m < VT / 4; ++m) {
+    const uint4 v = __ldg(src + tid + m * NT);
+    x[4 * m + 0] = v.x;
+    x[4 * m + 1] = v.y;
+    x[4 * m + 2] = v.z;
+    x[4 * m + 3] = v.w;
+  }
+  batcher_lab<VT, RM>(x, one, mone);
+#pragma unroll
+  for (int m = 1; m <= 5; ++m) {
+    const int g = 1 << m;
+    {
+      const bool upper = (lane & (g - 1)) >= (g >> 1);
+      const uint32_t uu = upper ? 1u : 0u;
+#pragma unroll
+      for (int q = 0; q < VT / 2; ++q) {
+        const uint32_t a = LM == 4 ? x[VT - 1 - q] + uu : __shfl_xor_sync(0xffffffffu, x[VT - 1 - q], g - 1);
+        const uint32_t b = LM == 4 ? x[q] + uu : __shfl_xor_sync(0xffffffffu, x[q], g - 1);
+        ce_lane<LM == 4 ? 0 : LM>(x[q], a, upper, uu, one);
+        ce_lane<LM == 4 ? 0 : LM>(x[VT - 1 - q], b, upper, uu, one);
+      }
+    }
+#pragma unroll
+    for (int st = g >> 2; st >= 1; st >>= 1) {
+      const bool upper = (lane & st) != 0;
+      const uint32_t uu = upper ? 1u : 0u;
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        ce_lane<LM == 4 ? 0 : LM>(x[q], LM == 4 ? x[q ^ 1] + uu : __shfl_xor_sync(0xffffffffu, x[q], st), upper, uu, one);
+    }
+#pragma unroll
+    for (int st = VT / 2; st >= 1; st >>= 1)
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        if ((q & st) == 0)
+          ce_reg<RM>(x[q], x[q + st], one, mone, q + (q >> 1) + (q >> 2) + (q >> 3) + (q >> 4));
+  }
+  const int p0 = tid * VT;
+  if constexpr (PASSES)
+    warp_sort_passes<32 * VT, NV, VT>(x, s, p0);
+  uint4 *dst = reinterpret_cast<uint4 *>(out + base + p0);
+#pragma unroll
+  for (int m = 0; m < VT / 4; ++m)
+    dst[m] = make_uint4(x[4 * m], x[4 * m + 1], x[4 * m + 2], x[4 * m + 3]);
+}
+
+__global__ void gen_kernel(uint32_t *x, uint64_t n, uint32_t seed) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    uint64_t z = (i + seed) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    x[i] = static_cast<uint32_t>(z ^ (z >> 31));
+  }
+}
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA error %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1);} } while (0)
+
+template <int NT, int VT, int RM, int LM, int PASSES>
+void run(const char *name, const uint32_t *in, uint32_t *out, uint64_t n, std::vector<uint32_t> &hin) {
+  constexpr int NV = NT * VT;
+  constexpr uint32_t smem = warp_sort_smem_bytes<NT, VT>();
+  auto k = lab_kernel<NT, VT, RM, LM, PASSES>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const unsigned blocks = static_cast<unsigned>(n / NV);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (int i = 0; i < 2; ++i)
+    k<<<blocks, NT, smem>>>(in, out, 1u);
+  CK(cudaDeviceSynchronize());
+  float best = 1e9f, sum = 0;
+  const int reps = 5;
+  for (int i = 0; i < reps; ++i) {
+    CK(cudaEventRecord(e0));
+    k<<<blocks, NT, smem>>>(in, out, 1u);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    best = std::min(best, ms);
+    sum += ms;
+  }
+  // verify the first and last 4 runs against std::sort
+  const int RUN = PASSES ? NV : 32 * VT;
+  bool ok = true;
+  std::vector<uint32_t> got(RUN), want(RUN);
+  for (uint64_t r : {uint64_t(0), uint64_t(1), n / RUN / 2, n / RUN - 1}) {
+    CK(cudaMemcpy(got.data(), out + r * RUN, RUN * 4ull, cudaMemcpyDeviceToHost));
+    // the kernel deals keys to threads in the load order; a run holds the
+    // keys of its own block range
+    const uint64_t blk = r * RUN / NV;
+    std::vector<uint32_t> blockkeys(hin.begin() + blk * NV, hin.begin() + (blk + 1) * NV);
+    if (PASSES) {
+      want = blockkeys;
+    } else {
+      // warp w of the block holds keys loaded by its lanes: element (m, tid) = in[4*(tid + m*NT) + c]
+      const int w = static_cast<int>((r * RUN % NV) / RUN);
+      want.clear();
+      for (int l = 0; l < 32; ++l)
+        for (int m = 0; m < VT / 4; ++m)
+          for (int c = 0; c < 4; ++c)
+            want.push_back(blockkeys[4 * ((w * 32 + l) + m * NT) + c]);
+    }
+    std::sort(want.begin(), want.end());
+    if (got != want)
+      ok = false;
+  }
+  printf("%-28s NT=%d VT=%d reg=%d lane=%d passes=%d  best %.3f ms  mean %.3f ms  (n=2^28; x4 for 2^30: %.2f ms)  %s\n",
+         name, NT, VT, RM, LM, PASSES, best, sum / reps, best * 4, ok ? "OK" : "MISMATCH");
+}
+
+int main() {
+  const uint64_t n = 1ull << 28;
+  uint32_t *in, *out;
+  CK(cudaMalloc(&in, n * 4));
+  CK(cudaMalloc(&out, n * 4));
+  gen_kernel<<<148 * 8, 256>>>(in, n, 12345u);
+  CK(cudaDeviceSynchronize());
+  std::vector<uint32_t> hin(n);
+  CK(cudaMemcpy(hin.data(), in, n * 4, cudaMemcpyDeviceToHost));
+  run<512, 32, 0, 0, 1>("baseline", in, out, n, hin);
+  run<512, 32, 0, 2, 1>("lane imad", in, out, n, hin);
+  run<512, 32, 4, 2, 1>("reg imad 1/4 + lane imad", in, out, n, hin);
+  run<512, 32, 5, 2, 1>("reg imad 1/3 + lane imad", in, out, n, hin);
+  run<512, 32, 6, 2, 1>("reg imad 1/2 + lane imad", in, out, n, hin);
+  run<512, 32, 2, 2, 1>("reg imad + lane imad", in, out, n, hin);
+  run<512, 32, 0, 0, 0>("baseline, no passes", in, out, n, hin);
+  run<512, 32, 0, 2, 0>("lane imad, no passes", in, out, n, hin);
+  run<512, 32, 4, 2, 0>("reg 1/4 + lane imad, no passes", in, out, n, hin);
+  run<512, 32, 5, 2, 0>("reg 1/3 + lane imad, no passes", in, out, n, hin);
+  run<512, 32, 6, 2, 0>("reg 1/2 + lane imad, no passes", in, out, n, hin);
+  return 0;
+}

@@ -828,3 +828,194 @@ __global__ void __launch_bounds__(NT, MINB)
     bulk_wait_read0();
 }
 
+
+
+// ===== K5g: conflict-free gathered outer merge (MP_QUAD_GATHER=1): correct, 3.04 vs 2.09 ms per pass =====
+// Round 2, session 5.  The fused pass with its outer merge (X with Y) done by
+// a bank-conflict-free gather into registers and a bitonic merge network
+// instead of a serial merge from shared memory.  Byte-exact (37 GPU sort
+// parity tests) but slower on B200: 2^30 u32 sort 33.9 vs 26.3 ms.  ncu
+// (profiles/r02/k5g/): the gather itself is conflict-free as designed (32
+// loads, 1 wavefront each, vs 3.5 for a serial merge's load) and all shared
+// loads drop 399 -> 343 M wavefronts per pass, but
+//   * 32 outputs per thread put neighbouring lanes' diagonals 32 apart, so
+//     the phase-2 split search probes X[16 l + c]: 16-way bank conflicts (6-7.5
+//     wavefronts per probe, 124 M wavefronts per pass -- more than the gather
+//     saved); probes would have to be re-aligned per lane;
+//   * the 32 sorted keys of a thread leave as eight 16-byte stores at a
+//     128-byte lane stride: 32 sectors per request, lg_throttle + drain
+//     stalls (staging them through shared memory needs a conflict-free
+//     blocked -> linear transpose, i.e. direction flags in the network);
+//   * 64 registers x 512 threads leave 2 CTAs = 1024 threads per SM (K5e:
+//     1280): the inner merges and the tile prologue, unchanged work, take
+//     0.5 ms longer per pass.
+// The ALU pipe (one warp instruction per 2 cycles per sub-partition) would
+// bound a fully gathered pass at ~13 ALU instructions per key and level --
+// no better than K5e's ~11 -- so the idea was retired rather than tuned.
+// Needs mp_bsort.cuh (order_u32, ce_u32) and the launch code below.
+//
+//   constexpr int kGatherNT = int(kQuadTile) / 32, kGatherVT = 33;
+//   constexpr uint32_t qsmem = quad_gather_smem_bytes<KT, kGatherNT, kGatherVT>();
+//   quad_tile_gather_kernel<KT, kGatherNT, kGatherVT><<<qtiles, kGatherNT, qsmem, s>>>(src, dst, n, w, lg4w, QT, QQ);
+// ---------------------------------------------------------------------------
+// K5g: K5e whose outer merge (X with Y) reads shared memory without bank
+// conflicts and has no dependent load chain.
+//
+// ncu on K5e (profiles/r02/k5e_full_raw.csv): the LSU data pipe runs at 81 %
+// of its wavefront peak and 277 M of the 399 M load wavefronts per pass are
+// bank conflicts -- every thread of a serial merge walks its own cursor, so a
+// warp's 32 loads fall on random banks (3.3 wavefronts per load).  K5g keeps
+// K5e's prologue and inner merges (VT = 33 outputs per thread, NT = 512) and
+// replaces the outer merge for full tiles (T = 32 * NT outputs):
+//   * phase 1 writes X forward from a 128-byte boundary (X[k] in bank k % 32)
+//     and Y REVERSED, ending in bank 31 (Y[k] in bank (31 - k) % 32), both as
+//     order-preserving u32 images;
+//   * thread i takes outputs [32 i, 32 i + 32): a Merge Path search gives its
+//     split a_s (its neighbour's is a_e), so it owns X[a_s, a_e) and
+//     Y[32 i - a_s, 32 (i + 1) - a_e) -- 32 elements whose banks are the 32
+//     consecutive residues (a_e - 32 .. a_e - 1) % 32: Y's descending part
+//     sits right below X's ascending part in bank space because the two
+//     cursors of a diagonal sum to a multiple of 32;
+//   * in load round j lane l fetches its element of bank (l + j) % 32 into
+//     register j: 32 loads, one wavefront each, all independent;
+//   * the registers then hold a rotation of (Y part descending, X part
+//     ascending) -- a bitonic sequence, which the five half-cleaner stages of
+//     a bitonic merge network sort whatever the rotation;
+//   * the 32 sorted outputs leave as eight 16-byte stores (no staging copy).
+// Bare keys only: equal keys are equal bytes, so the network's unstable order
+// is the stable merge's bytes.  Partial tiles and unaligned outputs take
+// K5e's path (quad_tile_merge).
+// ---------------------------------------------------------------------------
+template <class KT, int NT, int VT>
+__host__ __device__ constexpr uint32_t quad_gather_split_off() {
+  return (quad_smem_bytes<KT, NT, VT>() + 15u) & ~15u;
+}
+template <class KT, int NT, int VT>
+__host__ __device__ constexpr uint32_t quad_gather_smem_bytes() {
+  return quad_gather_split_off<KT, NT, VT>() + NT * 4u + 16u;
+}
+
+template <class KT, int NT, int VT>
+__global__ void __launch_bounds__(NT, 1024 / NT)
+    quad_tile_gather_kernel(const typename KT::T *__restrict__ src,
+                            typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
+                            uint32_t lg4w, uint32_t T, const QuadPt *__restrict__ Q) {
+  using T_ = typename KT::T;
+  static_assert(sizeof(T_) == 4, "bare 32-bit keys");
+  constexpr uint32_t KS = 4;
+  extern __shared__ __align__(128) char smem[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint32_t oW[4];
+  int cnt[4];
+  uint64_t o0;
+  quad_load_tile<KT, VT>(smem, src, n, w, lg4w, T, Q, oW, cnt, o0);
+  const int nx = cnt[0] + cnt[1], ny = cnt[2] + cnt[3], total = nx + ny;
+  if (total != 32 * NT || (reinterpret_cast<uintptr_t>(dst) & 15) != 0) {  // CTA-uniform
+    quad_tile_merge<KT, NT, VT>(smem, dst, oW, cnt, o0);
+    return;
+  }
+
+  // ---- phase 1: X = merge(R0w, R1w), Y = merge(R2w, R3w) as K5e ----
+  T_ keys[VT];
+  uint32_t vals[VT];
+  const int tx = (nx + VT - 1) / VT;
+  const int side = tid >= tx ? 1 : 0;
+  const int t1 = tid - side * tx;
+  const uint32_t oA = side ? oW[2] : oW[0], oB = side ? oW[3] : oW[1];
+  const int na = side ? cnt[2] : cnt[0], nb = side ? cnt[3] : cnt[1];
+  const int d1 = t1 * VT;
+  const bool act1 = d1 < na + nb;
+  if (act1) {
+    const int lo = split_predicted<KT, MP_QUAD_PRED_LOGW>(smem, oA, na, oB, nb, d1,
+                                          static_cast<float>(na) / static_cast<float>(na + nb));
+    serial_merge<KT, VT, false, true>(smem, oA, na, oB, nb, 0, 0, lo, d1 - lo, keys, vals);
+  }
+  __syncthreads();  // every window consumed
+  // X[k] at bX + 4k (bank k % 32); Y[k] at bY - 4k with bY in bank 31.  Each
+  // lies inside the span of the windows (and gaps) it was merged from: the
+  // alignment slack is < 128 bytes, two gaps are 2 * (4 VT + 20) bytes.
+  const uint32_t bX = (oW[0] + 127u) & ~127u;
+  const uint32_t bY = ((oW[2] + 4u * static_cast<uint32_t>(ny) + 127u - 128u) & ~127u) + 124u;
+  if (act1) {
+    const int lim = side ? ny : nx;
+    if (side == 0) {
+#pragma unroll
+      for (int k = 0; k < VT; ++k)
+        if (d1 + k < lim)
+          *reinterpret_cast<uint32_t *>(smem + bX + (d1 + k) * KS) = order_u32<KT>(keys[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < VT; ++k)
+        if (d1 + k < lim)
+          *reinterpret_cast<uint32_t *>(smem + bY - (d1 + k) * KS) = order_u32<KT>(keys[k]);
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2: thread tid owns outputs [32 tid, 32 tid + 32) ----
+  int *sp = reinterpret_cast<int *>(smem + quad_gather_split_off<KT, NT, VT>());
+  const int d2 = tid * 32;
+  int a_s;
+  {
+    const int lo = d2 > ny ? d2 - ny : 0;
+    const int hi = d2 < nx ? d2 : nx;
+    auto pred = [&](int m) {  // take Y at X index m on diagonal d2 (u32 order images)
+      return lds<uint32_t>(smem, bY - (d2 - 1 - m) * KS) < lds<uint32_t>(smem, bX + m * KS);
+    };
+    int l = lo, h = hi;
+    constexpr int LOGW = MP_QUAD_PRED_LOGW;
+    if (hi - lo > (2 << LOGW)) {
+      const float ratio = static_cast<float>(nx) / static_cast<float>(total);
+      const int guess = min(max(__float2int_rn(static_cast<float>(d2) * ratio), lo), hi);
+      const int lo0 = max(lo, guess - (1 << LOGW)), hi0 = min(hi, guess + (1 << LOGW));
+      const bool ok_lo = lo0 == lo || !pred(lo0 - 1);
+      const bool ok_hi = hi0 == hi || pred(hi0);
+      if (ok_lo && ok_hi) {
+        l = lo0;
+        h = hi0;
+      }
+    }
+    while (l < h) {
+      const int mid = (l + h) >> 1;
+      if (pred(mid))
+        h = mid;
+      else
+        l = mid + 1;
+    }
+    a_s = l;
+  }
+  sp[tid] = a_s;
+  __syncthreads();
+  const int a_e = tid + 1 < NT ? sp[tid + 1] : nx;
+  uint32_t x[32];
+  {
+    const int b_i = 32 - (a_e - a_s);  // Y elements of this block
+    const int base = a_e - 32;         // virtual index of the block's first element
+    const uint32_t c = static_cast<uint32_t>(lane - base) & 31u;
+    const uint32_t KA = bX + 4u * static_cast<uint32_t>(base);
+    const uint32_t KB = bY + 4u - 128u * static_cast<uint32_t>(tid) + 4u * static_cast<uint32_t>(base);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const uint32_t tj = (c + j) & 31u;
+      const uint32_t off = static_cast<int>(tj) >= b_i ? KA : KB;
+      x[j] = lds<uint32_t>(smem, off + 4u * tj);
+    }
+  }
+#pragma unroll
+  for (int st = 16; st >= 1; st >>= 1)
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      if ((q & st) == 0)
+        ce_u32(x[q], x[q + st]);
+  uint4 *out = reinterpret_cast<uint4 *>(dst + o0 + d2);
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    uint4 v;
+    v.x = static_cast<uint32_t>(from_order_u32<KT>(x[4 * m + 0]));
+    v.y = static_cast<uint32_t>(from_order_u32<KT>(x[4 * m + 1]));
+    v.z = static_cast<uint32_t>(from_order_u32<KT>(x[4 * m + 2]));
+    v.w = static_cast<uint32_t>(from_order_u32<KT>(x[4 * m + 3]));
+    out[m] = v;
+  }
+}
+
