@@ -144,6 +144,9 @@ __global__ void quad_partition_kernel(const typename KT::T *__restrict__ src,
 }
 
 // ---------------------------------------------------------------------------
+// (Round 2: K4q's two bounds and K4r's two inner splits searched in lockstep
+// -- independent loads of one step issued together -- K4q 70.5 -> 66 us,
+// K4r 117 -> 130 us per pass: not kept.)
 // K4r guess window (B200, 8 K4r launches of a 2^30 sort, ncu: 64 1061 us,
 // 128 986, 256 906, 512 1047, 1024 1186; sort 27.37 ms at 128, 27.29 at 256)
 #ifndef MP_K4R_GUESS_R
@@ -344,6 +347,12 @@ __host__ __device__ constexpr uint32_t quad_smem_bytes() {
 // Random-order merges deviate from the guess by O(sqrt(n)), so the window
 // usually holds; skewed inputs just take the fallback.  B200 (whole 2^30
 // sort): off 28.16 ms, window 2^5 28.59, 2^6 27.90-28.0, 2^7 28.06.
+// Round 2 (tools/ab_k5e_spec.sh, 2^30 sort 25.79 ms): neither fewer nor more
+// shared-memory loads per search helped -- bisecting inside the window first
+// and probing an edge only when the answer lands on it (4 of ~18 loads less,
+// the same in K3w's passes) 27.34 ms (K5e 2.09 -> 2.25 ms, K3w 7.63 -> 7.86);
+// probing the first one / two bisection levels together with the edges (one /
+// two dependent round trips less) 26.00 / 26.62 ms.
 #ifndef MP_QUAD_PRED_LOGW
 #define MP_QUAD_PRED_LOGW 6
 #endif
