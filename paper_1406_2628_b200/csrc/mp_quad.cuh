@@ -352,7 +352,11 @@ __host__ __device__ constexpr uint32_t quad_smem_bytes() {
 // and probing an edge only when the answer lands on it (4 of ~18 loads less,
 // the same in K3w's passes) 27.34 ms (K5e 2.09 -> 2.25 ms, K3w 7.63 -> 7.86);
 // probing the first one / two bisection levels together with the edges (one /
-// two dependent round trips less) 26.00 / 26.62 ms.
+// two dependent round trips less) 26.00 / 26.62 ms.  The same lazy edge
+// probes with the window recomputed after the loop (no extra live
+// registers): 25.74 ms, within noise of 25.79.  The window search as 7
+// unrolled binary-lifting steps with predicated probes (no loop counter or
+// branch, ~55 instructions less per search): 27.39 ms.
 #ifndef MP_QUAD_PRED_LOGW
 #define MP_QUAD_PRED_LOGW 6
 #endif
