@@ -3,7 +3,7 @@
 // Drop-in replacement for the reference's mergepath/sort.hpp
 // (/root/reference/proj/include/mergepath/sort.hpp) backed by the B200
 // library.  Both sorts are one call to mp_sort_host, which runs mp_sort's
-// schedule on the device: a block sort into sorted runs -- K3w (8192-key
+// schedule on the device: a block sort into sorted runs -- K3w (16384-key
 // runs, bare 32-bit keys: u32 / i32 / f32) or the stable K3 (2048-key runs:
 // values, 64-bit keys, element) -- then ceil(log2(N / run)) Merge Path
 // rounds, run as fused round pairs (one HBM pass per two rounds, mp_quad.cuh)

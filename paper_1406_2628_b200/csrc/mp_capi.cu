@@ -243,18 +243,21 @@ constexpr int kBlockVT = 16;
 constexpr uint64_t kRun = kBlockNT * kBlockVT;  // 2048-key block-sort runs
 // bare 32-bit keys: K3w (mp_bsort.cuh)
 #ifndef MP_WARP_NT
-#define MP_WARP_NT 512
+#define MP_WARP_NT 256
 #endif
 constexpr int kWarpNT = MP_WARP_NT;
-// K3w shape: 512 threads x 32 keys = 16384-key runs, so a 2^30-key sort is
-// 16 rounds = 8 fused round pairs with no plain round left over.  B200 A/B
-// (tools/ab_k3w_shape.sh, whole 2^30 sort / K3w alone, 1965 MHz): 512 x 16
-// (8192-key runs, 4 smem passes) 27.27 / 7.59 ms; 256 x 32 (8192-key runs,
-// 3 smem passes) 26.68 / 7.00 ms; 512 x 32 26.53 / 8.05 ms; 256 x 64
-// (16384-key runs, 3 smem passes, 80 registers, tools/ab_k3w_v64.sh) 26.27 /
-// 8.04 ms with K5e's granule copies vs 26.27-26.34 for 512 x 32: no gain.
+// K3w shape: 16384-key runs, so a 2^30-key sort is 16 rounds = 8 fused round
+// pairs with no plain round left over.  B200 A/B (tools/ab_k3w_shape.sh,
+// whole 2^30 sort / K3w alone, 1965 MHz): 512 x 16 (8192-key runs, 4 smem
+// passes) 27.27 / 7.59 ms; 256 x 32 (8192-key runs, 3 smem passes) 26.68 /
+// 7.00 ms; 512 x 32 26.53 / 8.05 ms; 256 x 64 (16384-key runs, 3 smem passes,
+// 80 registers, tools/ab_k3w_v64.sh) 26.27 / 8.04 ms with K5e's granule
+// copies vs 26.27-26.34 for 512 x 32.  With the FMA-pipe compare-exchanges
+// (mp_bsort.cuh) a register-network level costs ~0.4 ms against ~1 ms for a
+// shared-memory pass, and 256 x 64 (2048 keys per warp in registers, one pass
+// less) wins: 25.58 / 7.33 ms vs 25.78 / 7.54 for 512 x 32.
 #ifndef MP_K3W_VT
-#define MP_K3W_VT 32
+#define MP_K3W_VT 64
 #endif
 constexpr int kWarpVT = MP_K3W_VT;
 uint64_t warp_run() { return uint64_t(kWarpNT) * kWarpVT; }

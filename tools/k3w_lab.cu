@@ -87,7 +87,7 @@ __device__ __forceinline__ void batcher_lab(uint32_t (&x)[N], uint32_t one, uint
 }
 
 template <int NT, int VT, int RM, int LM, int PASSES>
-__global__ void __launch_bounds__(NT, 1024 / NT)
+__global__ void __launch_bounds__(NT, (VT == 64 ? 768 : 1024) / NT)
     lab_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint32_t one_) {
   constexpr int NV = NT * VT;
   extern __shared__ __align__(128) uint32_t s[];
@@ -218,15 +218,16 @@ int main() {
   std::vector<uint32_t> hin(n);
   CK(cudaMemcpy(hin.data(), in, n * 4, cudaMemcpyDeviceToHost));
   run<512, 32, 0, 0, 1>("baseline", in, out, n, hin);
-  run<512, 32, 0, 2, 1>("lane imad", in, out, n, hin);
-  run<512, 32, 4, 2, 1>("reg imad 1/4 + lane imad", in, out, n, hin);
-  run<512, 32, 5, 2, 1>("reg imad 1/3 + lane imad", in, out, n, hin);
-  run<512, 32, 6, 2, 1>("reg imad 1/2 + lane imad", in, out, n, hin);
-  run<512, 32, 2, 2, 1>("reg imad + lane imad", in, out, n, hin);
-  run<512, 32, 0, 0, 0>("baseline, no passes", in, out, n, hin);
-  run<512, 32, 0, 2, 0>("lane imad, no passes", in, out, n, hin);
-  run<512, 32, 4, 2, 0>("reg 1/4 + lane imad, no passes", in, out, n, hin);
-  run<512, 32, 5, 2, 0>("reg 1/3 + lane imad, no passes", in, out, n, hin);
-  run<512, 32, 6, 2, 0>("reg 1/2 + lane imad, no passes", in, out, n, hin);
+  run<512, 32, 6, 2, 1>("512x32 reg 1/2 + lane imad", in, out, n, hin);
+  run<256, 64, 0, 0, 1>("256x64 baseline", in, out, n, hin);
+  run<256, 64, 0, 2, 1>("256x64 lane imad", in, out, n, hin);
+  run<256, 64, 4, 2, 1>("256x64 reg 1/4 + lane imad", in, out, n, hin);
+  run<256, 64, 5, 2, 1>("256x64 reg 1/3 + lane imad", in, out, n, hin);
+  run<256, 64, 6, 2, 1>("256x64 reg 1/2 + lane imad", in, out, n, hin);
+  run<256, 64, 2, 2, 1>("256x64 reg imad + lane imad", in, out, n, hin);
+  run<512, 32, 6, 2, 0>("512x32 reg 1/2 + lane imad, no passes", in, out, n, hin);
+  run<256, 64, 6, 2, 0>("256x64 reg 1/2 + lane imad, no passes", in, out, n, hin);
+  run<256, 64, 5, 2, 0>("256x64 reg 1/3 + lane imad, no passes", in, out, n, hin);
+  run<256, 64, 0, 0, 0>("256x64 baseline, no passes", in, out, n, hin);
   return 0;
 }
