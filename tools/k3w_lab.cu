@@ -10,6 +10,8 @@
 //   LANE mode 0: x = upper ? max(x,y) : min(x,y)             (VIMNMX, 4 ALU)
 //   LANE mode 1: p = (y < x) ^ upper; @p mov x, y            (ISETP + predicated move; ptxas makes it SEL)
 //   LANE mode 2: p = (y < x) ^ upper; @p x = y*one + 0       (ISETP + predicated IMAD, 2 ALU + 2 FMA)
+//   LANE modes 3, 4, 5 are timing models with wrong results (shuffle + LOP3; no shuffles; the
+//   cross-lane stages of levels 3..5 as register stages, i.e. transposed levels minus the transposes)
 // Build:  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
 //         -I paper_1406_2628_b200/csrc -o tools/bin/k3w_lab tools/k3w_lab.cu
 #include <cstdio>
@@ -108,24 +110,34 @@ __global__ void __launch_bounds__(NT, (VT == 64 ? 768 : 1024) / NT)
 #pragma unroll
   for (int m = 1; m <= 5; ++m) {
     const int g = 1 << m;
-    {
+    if (LM == 5 && m >= 3) {
+      // timing model of the transposed levels: m register stages instead of the
+      // m cross-lane ones (same comparator count), no shuffles; the two
+      // shared-memory transposes per level are NOT included
+#pragma unroll
+      for (int t = 0; t < m; ++t)
+#pragma unroll
+        for (int q = 0; q < VT; ++q)
+          if ((q & (VT / 2 >> (t % 6))) == 0 && q + (VT / 2 >> (t % 6)) < VT)
+            ce_reg<RM>(x[q], x[q + (VT / 2 >> (t % 6))], one, mone, q + t);
+    } else {
       const bool upper = (lane & (g - 1)) >= (g >> 1);
       const uint32_t uu = upper ? 1u : 0u;
 #pragma unroll
       for (int q = 0; q < VT / 2; ++q) {
         const uint32_t a = LM == 4 ? x[VT - 1 - q] + uu : __shfl_xor_sync(0xffffffffu, x[VT - 1 - q], g - 1);
         const uint32_t b = LM == 4 ? x[q] + uu : __shfl_xor_sync(0xffffffffu, x[q], g - 1);
-        ce_lane<LM == 4 ? 0 : LM>(x[q], a, upper, uu, one);
-        ce_lane<LM == 4 ? 0 : LM>(x[VT - 1 - q], b, upper, uu, one);
+        ce_lane<(LM == 4) ? 0 : (LM == 5 ? 2 : LM)>(x[q], a, upper, uu, one);
+        ce_lane<(LM == 4) ? 0 : (LM == 5 ? 2 : LM)>(x[VT - 1 - q], b, upper, uu, one);
       }
     }
 #pragma unroll
-    for (int st = g >> 2; st >= 1; st >>= 1) {
+    for (int st = (LM == 5 && m >= 3) ? 0 : (g >> 2); st >= 1; st >>= 1) {
       const bool upper = (lane & st) != 0;
       const uint32_t uu = upper ? 1u : 0u;
 #pragma unroll
       for (int q = 0; q < VT; ++q)
-        ce_lane<LM == 4 ? 0 : LM>(x[q], LM == 4 ? x[q ^ 1] + uu : __shfl_xor_sync(0xffffffffu, x[q], st), upper, uu, one);
+        ce_lane<(LM == 4) ? 0 : (LM == 5 ? 2 : LM)>(x[q], LM == 4 ? x[q ^ 1] + uu : __shfl_xor_sync(0xffffffffu, x[q], st), upper, uu, one);
     }
 #pragma unroll
     for (int st = VT / 2; st >= 1; st >>= 1)
@@ -217,17 +229,9 @@ int main() {
   CK(cudaDeviceSynchronize());
   std::vector<uint32_t> hin(n);
   CK(cudaMemcpy(hin.data(), in, n * 4, cudaMemcpyDeviceToHost));
-  run<512, 32, 0, 0, 1>("baseline", in, out, n, hin);
-  run<512, 32, 6, 2, 1>("512x32 reg 1/2 + lane imad", in, out, n, hin);
-  run<256, 64, 0, 0, 1>("256x64 baseline", in, out, n, hin);
-  run<256, 64, 0, 2, 1>("256x64 lane imad", in, out, n, hin);
-  run<256, 64, 4, 2, 1>("256x64 reg 1/4 + lane imad", in, out, n, hin);
-  run<256, 64, 5, 2, 1>("256x64 reg 1/3 + lane imad", in, out, n, hin);
-  run<256, 64, 6, 2, 1>("256x64 reg 1/2 + lane imad", in, out, n, hin);
-  run<256, 64, 2, 2, 1>("256x64 reg imad + lane imad", in, out, n, hin);
-  run<512, 32, 6, 2, 0>("512x32 reg 1/2 + lane imad, no passes", in, out, n, hin);
   run<256, 64, 6, 2, 0>("256x64 reg 1/2 + lane imad, no passes", in, out, n, hin);
-  run<256, 64, 5, 2, 0>("256x64 reg 1/3 + lane imad, no passes", in, out, n, hin);
-  run<256, 64, 0, 0, 0>("256x64 baseline, no passes", in, out, n, hin);
+  run<256, 64, 6, 5, 0>("T: 256x64 levels 3-5 as register stages (no transposes), no passes", in, out, n, hin);
+  run<512, 32, 6, 2, 0>("512x32 reg 1/2 + lane imad, no passes", in, out, n, hin);
+  run<512, 32, 6, 5, 0>("T: 512x32 levels 3-5 as register stages (no transposes), no passes", in, out, n, hin);
   return 0;
 }
