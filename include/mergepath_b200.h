@@ -300,6 +300,16 @@ int mp_keyfile_load(const char *path, void *dev_keys, uint64_t capacity,
  * chunk k). */
 int mp_keyfile_store(const char *path, const void *dev_keys, uint64_t count,
                      int device, void *stream);
+/* File + file -> binary key file: the stable merge (MP_KEY_I64, ties to A)
+ * of two sorted key files, i.e. dataio's read_keys on both inputs,
+ * parallel_merge_into and write_keys_binary (dataio.cpp:33-98,
+ * mergebench.cpp:243-259) as one call whose stages overlap.  Binary inputs
+ * and the output are memory-mapped and streamed through mp_merge_host's
+ * pipeline: page-cache reads, H2D copies, chunk merges, D2H copies and the
+ * output's writes run concurrently.  Text inputs are parsed first.  *count
+ * (optional) = keys written.  Blocks until the output file is complete. */
+int mp_keyfile_merge(const char *path_a, const char *path_b, const char *path_out,
+                     uint64_t *count, int device);
 
 #ifdef __cplusplus
 }

