@@ -310,6 +310,11 @@ int mp_keyfile_store(const char *path, const void *dev_keys, uint64_t count,
  * (optional) = keys written.  Blocks until the output file is complete. */
 int mp_keyfile_merge(const char *path_a, const char *path_b, const char *path_out,
                      uint64_t *count, int device);
+/* File -> sorted binary key file (read_keys, parallel_merge_sort,
+ * write_keys_binary: mergebench.cpp:326-332) through mp_sort_host's pipeline
+ * on the mapped files. */
+int mp_keyfile_sort(const char *path_in, const char *path_out, uint64_t *count,
+                    int device);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,7 @@ SIGNATURES = [
     ("mp_keyfile_load", _i, [C.c_char_p, _p, _u64, _p, _i, _p]),
     ("mp_keyfile_store", _i, [C.c_char_p, _p, _u64, _i, _p]),
     ("mp_keyfile_merge", _i, [C.c_char_p, C.c_char_p, C.c_char_p, _p, _i]),
+    ("mp_keyfile_sort", _i, [C.c_char_p, C.c_char_p, _p, _i]),
     ("mp_key_size", _u64, [_i]),
     ("mp_partition", _i, [_i, _p, _u64, _p, _u64, _u64, _p, _p, _p]),
     ("mp_diagonal_search", _i, [_i, _p, _u64, _p, _u64, _p, _u64, _p, _p, _p]),

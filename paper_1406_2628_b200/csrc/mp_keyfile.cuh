@@ -485,4 +485,40 @@ int mp_keyfile_merge(const char *path_a, const char *path_b, const char *path_ou
   return rc;
 }
 
+// File -> sorted file (read_keys, parallel_merge_sort, write_keys_binary:
+// dataio.cpp:33-98, mergebench.cpp:326-332) through mp_sort_host's chunked
+// pipeline on the mapped files.
+int mp_keyfile_sort(const char *path_in, const char *path_out, uint64_t *count,
+                    int device) {
+  g_err.clear();
+  if (!path_in || !path_out)
+    return fail(MP_ERR_INVALID, "keyfile_sort: NULL path");
+  KeyfileSpan A;
+  if (int rc = A.open(path_in))
+    return rc;
+  const uint64_t n = A.n;
+  Fd out;
+  out.fd = ::open(path_out, O_RDWR | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+  if (out.fd < 0)
+    return io_fail("cannot open for writing", path_out);
+  const size_t out_bytes = kKeyfileHeader + n * 8;
+  if (::ftruncate(out.fd, static_cast<off_t>(out_bytes)) != 0)
+    return io_fail("cannot size", path_out);
+  void *om = ::mmap(nullptr, out_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, out.fd, 0);
+  if (om == MAP_FAILED)
+    return io_fail("cannot map", path_out);
+  unsigned char *head = static_cast<unsigned char *>(om);
+  std::memcpy(head, kKeyfileMagic, 8);
+  for (int i = 0; i < 8; ++i)
+    head[8 + i] = static_cast<unsigned char>(n >> (8 * i));
+  int rc = MP_OK;
+  if (n)
+    rc = mp_sort_host(MP_KEY_I64, A.keys, nullptr, n, head + kKeyfileHeader, nullptr, device);
+  if (::munmap(om, out_bytes) != 0 && rc == MP_OK)
+    rc = io_fail("unmap failed", path_out);
+  if (rc == MP_OK && count)
+    *count = n;
+  return rc;
+}
+
 }  // extern "C"

@@ -8,7 +8,7 @@
 //                          [--host-memory pinned|pageable] [--device N]
 //   mergebench_b200 sort   --in F [--variant plain|cache_efficient] [--threads ..]
 //                          [--cache-elems C] [--reps R] [--format json|csv] [--out F]
-//                          [--residency device|host] [--host-memory pinned|pageable] [--device N]
+//                          [--residency device|host|file [--sorted-out F]] [--host-memory pinned|pageable] [--device N]
 //   mergebench_b200 report --in F [--format json|csv] [--out F]
 //
 // Same subcommands, flags, report rows {op, variant, n, p, cache_elems, reps,
@@ -25,7 +25,8 @@
 // --residency host times the drop-in template call on host spans with a
 // steady clock, as the reference does (PCIe copies included); merge
 // --residency file times mp_keyfile_merge (key files in, merged key file
-// out, the ingest overlapped with the merge) and verifies the file.  p only
+// out, the ingest overlapped with the merge) and verifies the file; sort
+// --residency file likewise with mp_keyfile_sort.  p only
 // feeds the statistics, which are the reference's (device replays); the
 // GPU grid does not depend on it.  `cachesim` models a CPU cache and is not
 // part of this backend.
@@ -849,7 +850,10 @@ int run_sort(const Args &a) {
   const std::string format = opt(a, "format", "json");
   member("format", format, {"json", "csv"});
   const std::string residency = opt(a, "residency", "device");
-  member("residency", residency, {"device", "host"});
+  member("residency", residency, {"device", "host", "file"});
+  // file residency: each repetition is one mp_keyfile_sort (key file in,
+  // sorted key file out), read back and verified
+  const std::string fout = residency == "file" ? opt(a, "sorted-out", fin + ".sorted") : std::string();
   // host residency: page-lock the tool's vectors before timing (pinned) or
   // leave them pageable -- what a plain std::vector caller passes; the
   // library then stages the chunks through pinned slots
@@ -904,6 +908,15 @@ int run_sort(const Args &a) {
         }));
         out.resize(n);
         check_cuda(cudaMemcpy(out.data(), dOut->p, n * 8, cudaMemcpyDeviceToHost), "D2H");
+      } else if (residency == "file") {
+        std::uint64_t wrote = 0, got = 0;
+        times.push_back(wall([&] {
+          check_status(mp_keyfile_sort(fin.c_str(), fout.c_str(), &wrote, dev));
+        }));
+        out.assign(n, 0);
+        check_status(mp_keyfile_read(fout.c_str(), out.data(), n, &got));
+        if (wrote != n || got != n)
+          throw mismatch_error("sorted key file has the wrong length");
       } else {
         times.push_back(wall([&] {
           out = variant == "cache_efficient"
@@ -1002,7 +1015,7 @@ int main(int argc, char **argv) {
     if (cmd == "sort")
       return run_sort(parse_args(argc, argv, 2,
                                  {"in", "variant", "threads", "cache-elems", "reps",
-                                  "format", "out", "residency", "host-memory", "device"}));
+                                  "format", "out", "residency", "host-memory", "device", "sorted-out"}));
     if (cmd == "report")
       return run_report(parse_args(argc, argv, 2, {"in", "format", "out"}));
     if (cmd == "cachesim")

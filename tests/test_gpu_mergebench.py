@@ -68,7 +68,7 @@ def test_merge_segmented_register_csv(cuda, tmp_path):
     assert all(line.endswith(",true") and ",segmented," in line for line in lines[1:])
 
 
-@pytest.mark.parametrize("residency", ["device", "host"])
+@pytest.mark.parametrize("residency", ["device", "host", "file"])
 def test_sort_rows_verified(cuda, tmp_path, residency):
     rng = np.random.default_rng(5)
     x = rng.integers(-2**62, 2**62, 123_457, dtype=np.int64)
@@ -143,3 +143,22 @@ def test_keyfile_merge_file_to_file(cuda, port, tmp_path):
     with pytest.raises(OSError):
         N.check(N.lib.mp_keyfile_merge(str(tmp_path / "missing").encode(), str(fb).encode(),
                                        str(fo).encode(), None, 0))
+
+
+def test_keyfile_sort_file_to_file(cuda, port, tmp_path):
+    """mp_keyfile_sort: key file in, sorted key file out (mapped files through
+    mp_sort_host's pipeline), byte-identical to write_keys(oracle sort)."""
+    from paper_1406_2628_b200 import _native as N
+    from test_keyfile import write_keys
+    rng = np.random.default_rng(11)
+    for k, (x, binary) in enumerate([(rng.integers(-2**62, 2**62, 5_000_003), True),
+                                     (rng.integers(-3, 3, 70_001), False),
+                                     (np.zeros(0, dtype=np.int64), True)]):
+        fi, fo, fw = (tmp_path / f"{k}_{s}" for s in ("in", "out", "want"))
+        write_keys(fi, x, binary)
+        got = C.c_uint64()
+        N.check(N.lib.mp_keyfile_sort(str(fi).encode(), str(fo).encode(), C.byref(got), 0))
+        assert got.value == len(x)
+        want, _, _ = port.merge_sort("i64", x.astype(np.int64))
+        write_keys(fw, want, True)
+        assert fo.read_bytes() == fw.read_bytes(), k
