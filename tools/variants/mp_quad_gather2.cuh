@@ -9,6 +9,9 @@
 // 52 %, warps active 48 %: with 32 keys live per thread the kernel needs 64
 // registers, so an SM holds 2 x 512 threads (K5e: 2 x 640) and nothing hides
 // the tile prologue (19 % of the samples) and the store tail (11 %).
+// At 8192-output tiles (256 threads, 48 registers, 5 CTAs = 1280 threads per
+// SM, crossings still on the 16384 grid): 2.40 ms per pass, and K4r's twice as
+// many tile boundaries cost 0.28 instead of 0.12 ms: 29.3 ms per sort.
 // To build it: include this header after mp_quad.cuh in mp_capi.cu (-I
 // tools/variants) and launch, where K5e is launched for QT == kQuadTile,
 //   constexpr int GNT = int(kQuadTile) / 32, GVT = 33;
@@ -28,7 +31,7 @@ __host__ __device__ constexpr uint32_t quad_gather_smem_bytes() {
 }
 
 template <class KT, int NT, int VT>
-__global__ void __launch_bounds__(NT, 1024 / NT)
+__global__ void __launch_bounds__(NT, NT <= 256 ? 1280 / NT : 1024 / NT)
     quad_tile_gather_kernel(const typename KT::T *__restrict__ src,
                             typename KT::T *__restrict__ dst, uint64_t n, uint64_t w,
                             uint32_t lg4w, uint32_t T, const QuadPt *__restrict__ Q) {
