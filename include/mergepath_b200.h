@@ -307,7 +307,8 @@ int mp_keyfile_store(const char *path, const void *dev_keys, uint64_t count,
  * and the output are memory-mapped and streamed through mp_merge_host's
  * pipeline: page-cache reads, H2D copies, chunk merges, D2H copies and the
  * output's writes run concurrently.  Text inputs are parsed first.  *count
- * (optional) = keys written.  Blocks until the output file is complete. */
+ * (optional) = keys written.  Blocks until the output file is complete.
+ * The output must not be one of the inputs (MP_ERR_INVALID). */
 int mp_keyfile_merge(const char *path_a, const char *path_b, const char *path_out,
                      uint64_t *count, int device);
 /* File -> sorted binary key file (read_keys, parallel_merge_sort,

@@ -18,12 +18,15 @@ __all__ = ["mergepath"]
 
 
 def kernel_sources_sha256() -> str:
-    """SHA-256 over the kernel sources (csrc/*.cu, *.cuh): profiles stamped
-    with it (profiles/traffic_config*.json) are only used while it matches."""
+    """SHA-256 over the kernel sources (csrc/*.cu, *.cuh, except the key-file
+    I/O header, which holds no device code): profiles stamped with it
+    (profiles/traffic_config*.json) are only used while it matches."""
     import hashlib
     from pathlib import Path
     h = hashlib.sha256()
     for p in sorted((Path(__file__).resolve().parent / "csrc").glob("*.cu*")):
+        if p.name == "mp_keyfile.cuh":
+            continue
         h.update(p.name.encode())
         h.update(p.read_bytes())
     return h.hexdigest()

@@ -190,6 +190,15 @@ KeyfileStaging &keyfile_staging() {
 
 constexpr uint64_t kKeyfileChunk = 32ull << 20;  // bytes per staging buffer
 
+// true when `path` exists and is the file open as `fd` (same device and
+// inode): truncating it for output would pull the pages from under the
+// input's mapping
+bool same_file(int fd, const char *path) {
+  struct stat a, b;
+  return ::fstat(fd, &a) == 0 && ::stat(path, &b) == 0 && a.st_dev == b.st_dev &&
+         a.st_ino == b.st_ino;
+}
+
 // A key file's keys as a host span: a binary file is mapped (its keys start
 // 16 bytes into the page-aligned mapping, so they are 8-byte aligned), a
 // text file is parsed into `text`.
@@ -460,6 +469,8 @@ int mp_keyfile_merge(const char *path_a, const char *path_b, const char *path_ou
   if (int rc = B.open(path_b))
     return rc;
   const uint64_t n = A.n + B.n;
+  if (same_file(A.f.fd, path_out) || same_file(B.f.fd, path_out))
+    return fail(MP_ERR_INVALID, "keyfile_merge: the output file is one of the inputs: %s", path_out);
   Fd out;
   out.fd = ::open(path_out, O_RDWR | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
   if (out.fd < 0)
@@ -497,6 +508,8 @@ int mp_keyfile_sort(const char *path_in, const char *path_out, uint64_t *count,
   if (int rc = A.open(path_in))
     return rc;
   const uint64_t n = A.n;
+  if (same_file(A.f.fd, path_out))
+    return fail(MP_ERR_INVALID, "keyfile_sort: the output file is the input: %s", path_out);
   Fd out;
   out.fd = ::open(path_out, O_RDWR | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
   if (out.fd < 0)

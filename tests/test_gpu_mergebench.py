@@ -143,6 +143,13 @@ def test_keyfile_merge_file_to_file(cuda, port, tmp_path):
     with pytest.raises(OSError):
         N.check(N.lib.mp_keyfile_merge(str(tmp_path / "missing").encode(), str(fb).encode(),
                                        str(fo).encode(), None, 0))
+    before = fa.read_bytes()
+    with pytest.raises(ValueError, match="one of the inputs"):  # would truncate a mapped input
+        N.check(N.lib.mp_keyfile_merge(str(fa).encode(), str(fb).encode(), str(fa).encode(),
+                                       None, 0))
+    assert fa.read_bytes() == before
+    with pytest.raises(ValueError, match="is the input"):
+        N.check(N.lib.mp_keyfile_sort(str(fa).encode(), str(fa).encode(), None, 0))
 
 
 def test_keyfile_sort_file_to_file(cuda, port, tmp_path):
