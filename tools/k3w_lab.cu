@@ -89,7 +89,7 @@ __device__ __forceinline__ void batcher_lab(uint32_t (&x)[N], uint32_t one, uint
 }
 
 template <int NT, int VT, int RM, int LM, int PASSES>
-__global__ void __launch_bounds__(NT, (VT == 64 ? 768 : 1024) / NT)
+__global__ void __launch_bounds__(NT, (VT == 128 ? 384 : VT == 64 ? 768 : 1024) / NT)
     lab_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint32_t one_) {
   constexpr int NV = NT * VT;
   extern __shared__ __align__(128) uint32_t s[];
@@ -229,9 +229,9 @@ int main() {
   CK(cudaDeviceSynchronize());
   std::vector<uint32_t> hin(n);
   CK(cudaMemcpy(hin.data(), in, n * 4, cudaMemcpyDeviceToHost));
+  run<256, 64, 6, 2, 1>("256x64 reg 1/2 + lane imad", in, out, n, hin);
+  run<128, 128, 6, 2, 1>("128x128 reg 1/2 + lane imad", in, out, n, hin);
+  run<128, 128, 6, 2, 0>("128x128 reg 1/2 + lane imad, no passes", in, out, n, hin);
   run<256, 64, 6, 2, 0>("256x64 reg 1/2 + lane imad, no passes", in, out, n, hin);
-  run<256, 64, 6, 5, 0>("T: 256x64 levels 3-5 as register stages (no transposes), no passes", in, out, n, hin);
-  run<512, 32, 6, 2, 0>("512x32 reg 1/2 + lane imad, no passes", in, out, n, hin);
-  run<512, 32, 6, 5, 0>("T: 512x32 levels 3-5 as register stages (no transposes), no passes", in, out, n, hin);
   return 0;
 }
