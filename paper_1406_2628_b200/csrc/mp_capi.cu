@@ -1116,6 +1116,47 @@ bool is_pageable(const void *p) {
 }
 
 // Blocking parallel memcpy over persistent worker threads.
+// Host copy with non-temporal stores (SSE2, 64 bytes per iteration): a
+// staging copy's destination is read next by a DMA engine (pinned slot) or
+// not at all (the caller's output), so write-allocating it in the cache only
+// adds a read-for-ownership of every destination line to a copy that is
+// bound by host DRAM bandwidth.  glibc's memcpy switches to such stores only
+// above ~3/4 of the shared cache, far more than a pool part (1-4 MiB).
+// MP_HOST_COPY_NT=0 selects plain memcpy.
+#if defined(__x86_64__)
+#include <emmintrin.h>
+inline void stream_copy(char *dst, const char *src, size_t n) {
+  size_t head = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+  if (head > n)
+    head = n;
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  for (; n >= 64; n -= 64, dst += 64, src += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i *>(src + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i *>(dst), a);
+    _mm_stream_si128(reinterpret_cast<__m128i *>(dst + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i *>(dst + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i *>(dst + 48), d);
+  }
+  _mm_sfence();
+  std::memcpy(dst, src, n);
+}
+#else
+inline void stream_copy(char *dst, const char *src, size_t n) { std::memcpy(dst, src, n); }
+#endif
+inline bool host_copy_nt() {
+  static const bool v = [] {
+    const char *e = std::getenv("MP_HOST_COPY_NT");
+    return !(e && std::strcmp(e, "0") == 0);
+  }();
+  return v;
+}
+
 class CopyPool {
  public:
   static CopyPool &get() {
@@ -1184,7 +1225,10 @@ class CopyPool {
   void work() {
     size_t finished = 0;
     for (size_t i = next_.fetch_add(1); i < parts_.size(); i = next_.fetch_add(1)) {
-      std::memcpy(parts_[i].dst, parts_[i].src, parts_[i].bytes);
+      if (host_copy_nt())
+        stream_copy(parts_[i].dst, parts_[i].src, parts_[i].bytes);
+      else
+        std::memcpy(parts_[i].dst, parts_[i].src, parts_[i].bytes);
       ++finished;
     }
     if (finished) {
