@@ -88,7 +88,70 @@ __device__ __forceinline__ void batcher_lab(uint32_t (&x)[N], uint32_t one, uint
     ce_reg<RM>(x[net.a[m]], x[net.b[m]], one, mone, m);
 }
 
-template <int NT, int VT, int RM, int LM, int PASSES>
+// warp_sort_passes with the pass width as a runtime power of two: one copy
+// of the pass code for all log2(NT / 32) passes
+template <int NV, int VT>
+__device__ __forceinline__ void rolled_passes(uint32_t (&x)[VT], uint32_t *s, int p0) {
+  constexpr int SENT = VT > 32 ? VT : 32;
+#pragma unroll 1
+  for (int lgW = 5 + (VT == 64 ? 6 : VT == 32 ? 5 : 4); (1 << lgW) < NV; ++lgW) {
+    const int W = 1 << lgW, S = W + SENT;
+    {
+      const int r = p0 >> lgW, off = p0 & (W - 1);
+      uint32_t *p = s + pad32(r * S + off);
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        p[pad32(q)] = x[q];
+      if (off + VT == W) {
+        uint32_t *ps = s + pad32(r * S + W);
+#pragma unroll
+        for (int q = 0; q < VT; ++q)
+          ps[pad32(q)] = 0xFFFFFFFFu;
+      }
+    }
+    __syncthreads();
+    const int diag = p0 & (2 * W - 1);
+    const int aO = (p0 >> (lgW + 1)) * 2 * S;
+    const int bO = aO + S;
+    int lo = diag > W ? diag - W : 0;
+    int hi = diag < W ? diag : W;
+    {
+      const int R = W <= 1024 ? MP_K3W_PRED_R0 : MP_K3W_PRED_R1;
+      if (hi - lo > 2 * R) {
+        const int g = diag >> 1;
+        const int lo0 = max(lo, g - R), hi0 = min(hi, g + R);
+        const bool ok_lo = lo0 == lo || !(s[pad32(bO + diag - lo0)] < s[pad32(aO + lo0 - 1)]);
+        const bool ok_hi = hi0 == hi || (s[pad32(bO + diag - 1 - hi0)] < s[pad32(aO + hi0)]);
+        if (ok_lo && ok_hi) {
+          lo = lo0;
+          hi = hi0;
+        }
+      }
+    }
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s[pad32(bO + diag - 1 - mid)] < s[pad32(aO + mid)])
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    int pa = aO + lo, pb = bO + (diag - lo);
+    uint32_t ka = s[pad32(pa)], kb = s[pad32(pb)];
+#pragma unroll
+    for (int q = 0; q < VT; ++q) {
+      const bool tb = kb < ka;
+      x[q] = min(ka, kb);
+      pa += tb ? 0 : 1;
+      pb += tb ? 1 : 0;
+      const uint32_t nx = s[pad32(tb ? pb : pa)];
+      kb = tb ? nx : kb;
+      ka = tb ? ka : nx;
+    }
+    __syncthreads();
+  }
+}
+
+template <int NT, int VT, int RM, int LM, int PASSES, bool ROLL = false>
 __global__ void __launch_bounds__(NT, (VT == 128 ? 384 : VT == 64 ? 768 : 1024) / NT)
     lab_kernel(const uint32_t *__restrict__ in, uint32_t *__restrict__ out, uint32_t one_) {
   constexpr int NV = NT * VT;
@@ -107,6 +170,38 @@ __global__ void __launch_bounds__(NT, (VT == 128 ? 384 : VT == 64 ? 768 : 1024) 
     x[4 * m + 3] = v.w;
   }
   batcher_lab<VT, RM>(x, one, mone);
+  if constexpr (ROLL) {
+    // the five warp levels as one rolled loop (runtime shuffle masks): the
+    // fully unrolled K3w is ~9700 instructions = 155 KB of code, more than
+    // the instruction caches hold (ncu: no_instruction stalls)
+#pragma unroll 1
+    for (int m = 1; m <= 5; ++m) {
+      const int g = 1 << m;
+      {
+        const uint32_t uu = (lane & (g - 1)) >= (g >> 1) ? 1u : 0u;
+#pragma unroll
+        for (int q = 0; q < VT / 2; ++q) {
+          const uint32_t a = __shfl_xor_sync(0xffffffffu, x[VT - 1 - q], g - 1);
+          const uint32_t b = __shfl_xor_sync(0xffffffffu, x[q], g - 1);
+          ce_lane<2>(x[q], a, uu != 0, uu, one);
+          ce_lane<2>(x[VT - 1 - q], b, uu != 0, uu, one);
+        }
+      }
+#pragma unroll 1
+      for (int st = g >> 2; st >= 1; st >>= 1) {
+        const uint32_t uu = (lane & st) != 0 ? 1u : 0u;
+#pragma unroll
+        for (int q = 0; q < VT; ++q)
+          ce_lane<2>(x[q], __shfl_xor_sync(0xffffffffu, x[q], st), uu != 0, uu, one);
+      }
+#pragma unroll
+      for (int st = VT / 2; st >= 1; st >>= 1)
+#pragma unroll
+        for (int q = 0; q < VT; ++q)
+          if ((q & st) == 0)
+            ce_reg<RM>(x[q], x[q + st], one, mone, q + (q >> 1) + (q >> 2) + (q >> 3) + (q >> 4));
+    }
+  } else
 #pragma unroll
   for (int m = 1; m <= 5; ++m) {
     const int g = 1 << m;
@@ -147,7 +242,9 @@ __global__ void __launch_bounds__(NT, (VT == 128 ? 384 : VT == 64 ? 768 : 1024) 
           ce_reg<RM>(x[q], x[q + st], one, mone, q + (q >> 1) + (q >> 2) + (q >> 3) + (q >> 4));
   }
   const int p0 = tid * VT;
-  if constexpr (PASSES)
+  if constexpr (PASSES == 2)
+    rolled_passes<NV, VT>(x, s, p0);
+  else if constexpr (PASSES)
     warp_sort_passes<32 * VT, NV, VT>(x, s, p0);
   uint4 *dst = reinterpret_cast<uint4 *>(out + base + p0);
 #pragma unroll
@@ -166,11 +263,11 @@ __global__ void gen_kernel(uint32_t *x, uint64_t n, uint32_t seed) {
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA error %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1);} } while (0)
 
-template <int NT, int VT, int RM, int LM, int PASSES>
+template <int NT, int VT, int RM, int LM, int PASSES, bool ROLL = false>
 void run(const char *name, const uint32_t *in, uint32_t *out, uint64_t n, std::vector<uint32_t> &hin) {
   constexpr int NV = NT * VT;
   constexpr uint32_t smem = warp_sort_smem_bytes<NT, VT>();
-  auto k = lab_kernel<NT, VT, RM, LM, PASSES>;
+  auto k = lab_kernel<NT, VT, RM, LM, PASSES, ROLL>;
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const unsigned blocks = static_cast<unsigned>(n / NV);
   cudaEvent_t e0, e1;
@@ -192,7 +289,7 @@ void run(const char *name, const uint32_t *in, uint32_t *out, uint64_t n, std::v
     sum += ms;
   }
   // verify the first and last 4 runs against std::sort
-  const int RUN = PASSES ? NV : 32 * VT;
+  const int RUN = PASSES ? NV : 32 * VT;  // PASSES: 1 = unrolled per width, 2 = rolled
   bool ok = true;
   std::vector<uint32_t> got(RUN), want(RUN);
   for (uint64_t r : {uint64_t(0), uint64_t(1), n / RUN / 2, n / RUN - 1}) {
@@ -230,8 +327,8 @@ int main() {
   std::vector<uint32_t> hin(n);
   CK(cudaMemcpy(hin.data(), in, n * 4, cudaMemcpyDeviceToHost));
   run<256, 64, 6, 2, 1>("256x64 reg 1/2 + lane imad", in, out, n, hin);
-  run<128, 128, 6, 2, 1>("128x128 reg 1/2 + lane imad", in, out, n, hin);
-  run<128, 128, 6, 2, 0>("128x128 reg 1/2 + lane imad, no passes", in, out, n, hin);
-  run<256, 64, 6, 2, 0>("256x64 reg 1/2 + lane imad, no passes", in, out, n, hin);
+  run<256, 64, 6, 2, 1, true>("256x64 rolled warp levels", in, out, n, hin);
+  run<256, 64, 6, 2, 2, true>("256x64 rolled warp levels + rolled passes", in, out, n, hin);
+  run<256, 64, 6, 2, 2, false>("256x64 rolled passes only", in, out, n, hin);
   return 0;
 }
