@@ -88,6 +88,77 @@ __device__ __forceinline__ void batcher_lab(uint32_t (&x)[N], uint32_t one, uint
     ce_reg<RM>(x[net.a[m]], x[net.b[m]], one, mone, m);
 }
 
+// warp_sort_passes with two independent merge chains per thread (outputs
+// [p0, p0 + VT/2) and [p0 + VT/2, p0 + VT): a second split search, two
+// dependent load chains in flight)
+template <int W, int NV, int VT>
+__device__ __forceinline__ void passes_ilp2(uint32_t (&x)[VT], uint32_t *s, int p0) {
+  if constexpr (W < NV) {
+    constexpr int S = W + (VT > 32 ? VT : 32);
+    {
+      const int r = p0 / W, off = p0 % W;
+      uint32_t *p = s + pad32(r * S + off);
+#pragma unroll
+      for (int q = 0; q < VT; ++q)
+        p[pad32(q)] = x[q];
+      if (off + VT == W) {
+        uint32_t *ps = s + pad32(r * S + W);
+#pragma unroll
+        for (int q = 0; q < VT; ++q)
+          ps[pad32(q)] = 0xFFFFFFFFu;
+      }
+    }
+    __syncthreads();
+    const int aO = (p0 / (2 * W)) * 2 * S;
+    const int bO = aO + S;
+    auto split = [&](int diag) {
+      int lo = diag > W ? diag - W : 0;
+      int hi = diag < W ? diag : W;
+      constexpr int R = W <= 1024 ? MP_K3W_PRED_R0 : MP_K3W_PRED_R1;
+      if (hi - lo > 2 * R) {
+        const int g = diag >> 1;
+        const int lo0 = max(lo, g - R), hi0 = min(hi, g + R);
+        const bool ok_lo = lo0 == lo || !(s[pad32(bO + diag - lo0)] < s[pad32(aO + lo0 - 1)]);
+        const bool ok_hi = hi0 == hi || (s[pad32(bO + diag - 1 - hi0)] < s[pad32(aO + hi0)]);
+        if (ok_lo && ok_hi) {
+          lo = lo0;
+          hi = hi0;
+        }
+      }
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s[pad32(bO + diag - 1 - mid)] < s[pad32(aO + mid)])
+          hi = mid;
+        else
+          lo = mid + 1;
+      }
+      return lo;
+    };
+    const int d0 = p0 % (2 * W), d1 = d0 + VT / 2;
+    const int l0 = split(d0), l1 = split(d1);
+    int pa0 = aO + l0, pb0 = bO + (d0 - l0), pa1 = aO + l1, pb1 = bO + (d1 - l1);
+    uint32_t ka0 = s[pad32(pa0)], kb0 = s[pad32(pb0)], ka1 = s[pad32(pa1)], kb1 = s[pad32(pb1)];
+#pragma unroll
+    for (int q = 0; q < VT / 2; ++q) {
+      const bool t0 = kb0 < ka0, t1 = kb1 < ka1;
+      x[q] = min(ka0, kb0);
+      x[q + VT / 2] = min(ka1, kb1);
+      pa0 += t0 ? 0 : 1;
+      pb0 += t0 ? 1 : 0;
+      pa1 += t1 ? 0 : 1;
+      pb1 += t1 ? 1 : 0;
+      const uint32_t n0 = s[pad32(t0 ? pb0 : pa0)];
+      const uint32_t n1 = s[pad32(t1 ? pb1 : pa1)];
+      kb0 = t0 ? n0 : kb0;
+      ka0 = t0 ? ka0 : n0;
+      kb1 = t1 ? n1 : kb1;
+      ka1 = t1 ? ka1 : n1;
+    }
+    __syncthreads();
+    passes_ilp2<2 * W, NV, VT>(x, s, p0);
+  }
+}
+
 // warp_sort_passes with the pass width as a runtime power of two: one copy
 // of the pass code for all log2(NT / 32) passes
 template <int NV, int VT>
@@ -242,7 +313,9 @@ __global__ void __launch_bounds__(NT, (VT == 128 ? 384 : VT == 64 ? 768 : 1024) 
           ce_reg<RM>(x[q], x[q + st], one, mone, q + (q >> 1) + (q >> 2) + (q >> 3) + (q >> 4));
   }
   const int p0 = tid * VT;
-  if constexpr (PASSES == 2)
+  if constexpr (PASSES == 3)
+    passes_ilp2<32 * VT, NV, VT>(x, s, p0);
+  else if constexpr (PASSES == 2)
     rolled_passes<NV, VT>(x, s, p0);
   else if constexpr (PASSES)
     warp_sort_passes<32 * VT, NV, VT>(x, s, p0);
@@ -327,8 +400,8 @@ int main() {
   std::vector<uint32_t> hin(n);
   CK(cudaMemcpy(hin.data(), in, n * 4, cudaMemcpyDeviceToHost));
   run<256, 64, 6, 2, 1>("256x64 reg 1/2 + lane imad", in, out, n, hin);
-  run<256, 64, 6, 2, 1, true>("256x64 rolled warp levels", in, out, n, hin);
-  run<256, 64, 6, 2, 2, true>("256x64 rolled warp levels + rolled passes", in, out, n, hin);
-  run<256, 64, 6, 2, 2, false>("256x64 rolled passes only", in, out, n, hin);
+  run<256, 64, 6, 2, 3>("256x64 passes with two merge chains", in, out, n, hin);
+  run<512, 32, 6, 2, 1>("512x32 reg 1/2 + lane imad", in, out, n, hin);
+  run<512, 32, 6, 2, 3>("512x32 passes with two merge chains", in, out, n, hin);
   return 0;
 }
